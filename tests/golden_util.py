@@ -1,0 +1,24 @@
+"""Load the golden fixtures written by oracle/make_golden.py."""
+import glob
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def load(name):
+    with np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    for k in ("kind", "rule"):
+        d[k] = str(d[k])
+    for k in ("p", "nq"):
+        d[k] = int(d[k])
+    d["alpha"] = float(d["alpha"])
+    for k in ("clamped", "res_clamped", "D_clamped"):
+        d[k] = bool(d[k])
+    return d
