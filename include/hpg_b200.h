@@ -1,0 +1,115 @@
+/*
+ * hpg_b200.h -- C ABI of the B200 (sm_100a) element-quadrature engine for the
+ * hierarchical proximal Galerkin (hpG) LVPP saddle system.
+ *
+ * The reference (pure Python, /root/reference/pkg/src/hpgalerkin) has no FFI;
+ * its seam is duck typing on the `disc` object.  Each entry point below
+ * replaces one reference callable; the Python host
+ * (paper_2412_13733_b200/disc.py) binds them with ctypes and keeps the
+ * reference's method names, argument meaning and return arrays.
+ *
+ * Conventions
+ *  - All array pointers are caller-owned DEVICE memory (fp64 unless stated);
+ *    `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *  - psi-side vectors are in the reference's GLOBAL order: the x-major tensor
+ *    order of PsiSpace2D (spaces.py:212-214), i.e. a (ncx*n) x (ncy*n)
+ *    row-major array; gradient vectors stack [psi_x ; psi_y]
+ *    (assembly.py:744-745).
+ *  - u-side vectors are interior U coefficients (spaces.py:188-189): a
+ *    (nix x niy) row-major array, nix = ncx*p - 1.
+ *  - Cell order (blocks, point samples) is (cx, cy) cx-major
+ *    (assembly.py:482).  Point samples are (ncells, nq, nq) row-major.
+ *  - Every call returns 0 on success, a nonzero HPG_ERR_* code otherwise;
+ *    hpgLastError() gives a message.  Calls are asynchronous on `stream`.
+ *  - Clamp flags (`clamped`) are device ints; the call ORs 1 into *clamped
+ *    when exp(-v) overflows the reference's clamp (assembly.py:187-192);
+ *    the caller zeroes it.
+ */
+#ifndef HPG_B200_H
+#define HPG_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPG_OK 0
+#define HPG_ERR_ARG 1
+#define HPG_ERR_CUDA 2
+#define HPG_ERR_UNSUPPORTED 3
+
+#define HPG_OBSTACLE 0
+#define HPG_GRADIENT 1
+
+typedef struct hpgPlan_st* hpgPlan;
+
+/* Tables + mesh geometry of one uniform-degree discretisation.
+ * Replaces the per-cell CellKernel2D construction (assembly.py:232-238,
+ * 483-488 / 736-741).  S: nq x n, T: n x nq (psi side), Su: nq x (p+1),
+ * Tu: (p+1) x nq (u side), hx: ncx widths, hy: ncy widths -- HOST arrays,
+ * copied.  n = p-1 (obstacle) or p (gradient). */
+int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq,
+                  const double* S, const double* T, const double* Su,
+                  const double* Tu, const double* hx, const double* hy);
+int hpgPlanDestroy(hpgPlan plan);
+/* info[0..9] = n, m, nq, ncells, ndof_psi, ndof_u, wcache_doubles,
+ *              block_doubles_per_cell, path(0 warp, 1 cta), splits */
+int hpgPlanInfo(hpgPlan plan, long long* info);
+
+/* ObstacleDisc2D.exp_moments (assembly.py:541-548).  out[ndof_psi].
+ * wcache (nullable, info[6] doubles): the clamped exp weights, consumed by
+ * hpgApplyCached / hpgBlocks*. */
+int hpgObstacleMoments(hpgPlan plan, const double* psi, double* out,
+                       int* clamped, double* wcache, void* stream);
+/* ObstacleDisc2D.apply_D (assembly.py:559-567): y = D(psi) x. */
+int hpgObstacleApplyD(hpgPlan plan, const double* psi, const double* x,
+                      double* y, void* stream);
+/* GradientDisc2D.nl_moments (assembly.py:781-791); phi: point samples. */
+int hpgGradientMoments(hpgPlan plan, const double* psi, const double* phi,
+                       double* out, double* wcache, void* stream);
+/* GradientDisc2D.apply_D (assembly.py:817-832). */
+int hpgGradientApplyD(hpgPlan plan, const double* psi, const double* phi,
+                      const double* x, double* y, void* stream);
+/* Jacobian action from cached point weights (written by a moments/residual
+ * call at the same psi): equals apply_D and CellBlockMatrix @ x
+ * (assembly.py:281-285) for the D of that psi. */
+int hpgApplyCached(hpgPlan plan, const double* wcache, const double* x,
+                   double* y, void* stream);
+
+/* proximal.residual (proximal.py:112-126), fused:
+ *   b_u   = alpha f_load + B psi_prev - alpha A u - B psi
+ *   b_psi = phi_moments - B^T u - exp_moments(psi)      (obstacle)
+ *         = nl_moments(psi) - B^T u                     (gradient)
+ * phi = phi_moments [ndof_psi] (obstacle) or point samples (gradient). */
+int hpgResidual(hpgPlan plan, double alpha, const double* psi_prev,
+                const double* u, const double* psi, const double* phi,
+                const double* f_load, double* b_u, double* b_psi,
+                int* clamped, double* wcache, void* stream);
+
+/* Element blocks (assembly.py:550-557 / 804-815) from cached weights:
+ * blocks[ncells][nb][nb], nb = n^2 (obstacle) or 2 n^2 (gradient),
+ * row = a*n+b (test), col = j*n+k (trial).  Cells [c0, c0+count). */
+int hpgBlocks(hpgPlan plan, const double* wcache, double* blocks, int c0,
+              int count, void* stream);
+/* CellBlockMatrix.matvec (assembly.py:281-285) on device blocks. */
+int hpgBlocksMatvec(hpgPlan plan, const double* blocks, const double* x,
+                    double* y, void* stream);
+
+/* Exact u-side couplings (assembly.py:81-116, 470-477, 725-729). */
+int hpgBTu(hpgPlan plan, const double* u, double* out, void* stream);
+int hpgBPsi(hpgPlan plan, const double* psi, double* out, void* stream);
+int hpgAu(hpgPlan plan, const double* u, double* out, void* stream);
+
+/* Data terms from point samples (ncells, nq, nq):
+ * moments_from_values / data_moments (assembly.py:514-533) and
+ * load_vector (assembly.py:502-512). */
+int hpgMomentsFromValues(hpgPlan plan, const double* vals, double* out,
+                         void* stream);
+int hpgLoadVector(hpgPlan plan, const double* vals, double* out, void* stream);
+
+const char* hpgLastError(void);
+int hpgVersion(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

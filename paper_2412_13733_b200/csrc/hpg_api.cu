@@ -1,0 +1,441 @@
+// C ABI of the B200 hpG element-quadrature engine (see include/hpg_b200.h).
+// Host side of the library: plan construction (fragment-ordered tables on the
+// device), path selection and kernel launches.  No allocation in the hot
+// entry points: every workspace is sized at plan creation.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hpg_b200.h"
+#include "hpg_blocks.cuh"
+#include "hpg_common.cuh"
+#include "hpg_launch.cuh"
+#include "hpg_useside.cuh"
+
+using namespace hpg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t _e = (x);                                                               \
+    if (_e != cudaSuccess)                                                              \
+      return fail(HPG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+#define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
+
+// PK(X)[tile][ks][lane] = X[8*tile + r][8*(ks>>1) + 2c + (ks&1)], zero padded.
+std::vector<double> pk_table(const double* X, int rows, int cols, int RT, int KP) {
+  std::vector<double> out((size_t)RT * (KP / 4) * 32, 0.0);
+  for (int t = 0; t < RT; ++t)
+    for (int ks = 0; ks < KP / 4; ++ks)
+      for (int lane = 0; lane < 32; ++lane) {
+        int r = lane >> 2, c = lane & 3;
+        int row = 8 * t + r, col = 8 * (ks >> 1) + 2 * c + (ks & 1);
+        double v = (row < rows && col < cols) ? X[(size_t)row * cols + col] : 0.0;
+        out[((size_t)t * (KP / 4) + ks) * 32 + lane] = v;
+      }
+  return out;
+}
+
+template <typename T>
+int upload(T** dst, const T* src, size_t count) {
+  CUDA_TRY(cudaMalloc(dst, count * sizeof(T) + 16));
+  CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  return HPG_OK;
+}
+
+}  // namespace
+
+namespace hpg {
+int set_error(int code, const char* where, cudaError_t e) {
+  return fail(code, std::string(where) + ": " + cudaGetErrorString(e));
+}
+int set_error_msg(int code, const char* msg) { return fail(code, msg); }
+}  // namespace hpg
+
+struct hpgPlan_st {
+  int kind, ncx, ncy, p, n, m, nq, N;
+  int NT, QT, NP, QP;
+  int nix, niy;
+  long long ncomp, ndof_psi, ndof_u;
+  int use_warp[8];
+  int splits;
+  double *Sf = nullptr, *Tf = nullptr, *hx = nullptr, *hy = nullptr;
+  double* G = nullptr;        // block table [n2][QP]
+  // u-side analysis (load_vector): PK(Tu) with n := m
+  int NTu;
+  double* Tuf = nullptr;
+  double* Suf = nullptr;
+  double* scratch_u = nullptr;  // [N][m][m]
+  double* mu = nullptr;         // x-major m-tiles
+  double* partial = nullptr;    // CTA split partials
+  size_t partial_len = 0;
+  double* Z = nullptr;          // blocks stage-1 scratch
+  int zcells = 0;
+  int* dflag = nullptr;
+  int nsm = 148;
+};
+
+namespace {
+
+ElemArgs base_args(const hpgPlan_st* P) {
+  ElemArgs A;
+  memset(&A, 0, sizeof(A));
+  A.ncx = P->ncx; A.ncy = P->ncy; A.n = P->n; A.m = P->m; A.p = P->p; A.nq = P->nq; A.N = P->N;
+  A.nix = P->nix; A.niy = P->niy;
+  A.ld = (long long)P->ncy * P->n;
+  A.ncomp = P->ncomp;
+  A.hx = P->hx; A.hy = P->hy;
+  A.Sf = P->Sf; A.Tf = P->Tf;
+  A.NT = P->NT; A.QT = P->QT; A.splits = 1;
+  A.partial = P->partial;
+  return A;
+}
+
+bool warp_fits(int mode, int NT, int QT) {
+  switch (mode) {
+    case M_OBST_RES: return warp_available<M_OBST_RES>(NT, QT);
+    case M_OBST_APPLY: return warp_available<M_OBST_APPLY>(NT, QT);
+    case M_OBST_CACHED: return warp_available<M_OBST_CACHED>(NT, QT);
+    case M_GRAD_RES: return warp_available<M_GRAD_RES>(NT, QT);
+    case M_GRAD_APPLY: return warp_available<M_GRAD_APPLY>(NT, QT);
+    case M_GRAD_CACHED: return warp_available<M_GRAD_CACHED>(NT, QT);
+    default: return false;
+  }
+}
+
+template <int MODE>
+int run_elem(hpgPlan_st* P, ElemArgs A, cudaStream_t s) {
+  if (!P->use_warp[MODE]) A.splits = P->splits;
+  return run_mode<MODE>(P->use_warp[MODE] != 0, A, s);
+}
+
+int check(hpgPlan p) {
+  if (p == nullptr) return fail(HPG_ERR_ARG, "null plan");
+  return HPG_OK;
+}
+
+int run_ulocal(hpgPlan_st* P, UArgs& U, cudaStream_t s) {
+  long long total = (long long)P->N * P->m * P->m;
+  k_u_local<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U);
+  LAUNCH_CHECK();
+  long long tot2 = (long long)P->nix * P->niy;
+  if (tot2 > 0) {
+    k_u_gather<<<(unsigned)((tot2 + 255) / 256), 256, 0, s>>>(U);
+    LAUNCH_CHECK();
+  }
+  return HPG_OK;
+}
+
+UArgs base_uargs(const hpgPlan_st* P) {
+  UArgs U;
+  memset(&U, 0, sizeof(U));
+  U.ncx = P->ncx; U.ncy = P->ncy; U.p = P->p; U.n = P->n; U.m = P->m;
+  U.nix = P->nix; U.niy = P->niy; U.gradient = P->kind == HPG_GRADIENT;
+  U.ld = (long long)P->ncy * P->n; U.ncomp = P->ncomp;
+  U.hx = P->hx; U.hy = P->hy;
+  U.scratch = P->scratch_u;
+  return U;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpgVersion(void) { return 1; }
+
+const char* hpgLastError(void) { return g_err.c_str(); }
+
+int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, const double* S,
+                  const double* T, const double* Su, const double* Tu, const double* hx,
+                  const double* hy) {
+  if (plan == nullptr) return fail(HPG_ERR_ARG, "null plan pointer");
+  *plan = nullptr;
+  if (kind != HPG_OBSTACLE && kind != HPG_GRADIENT) return fail(HPG_ERR_ARG, "unknown kind");
+  if (ncx < 1 || ncy < 1 || nq < 1) return fail(HPG_ERR_ARG, "bad mesh or quadrature size");
+  if (kind == HPG_OBSTACLE && p < 2) return fail(HPG_ERR_ARG, "obstacle discretization requires p >= 2");
+  if (kind == HPG_GRADIENT && p < 1) return fail(HPG_ERR_ARG, "gradient discretization requires p >= 1");
+  if (!S || !T || !Su || !Tu || !hx || !hy) return fail(HPG_ERR_ARG, "null table");
+  hpgPlan_st* P = new hpgPlan_st();
+  P->kind = kind; P->ncx = ncx; P->ncy = ncy; P->p = p; P->nq = nq;
+  P->n = kind == HPG_OBSTACLE ? p - 1 : p;
+  P->m = p + 1;
+  P->N = ncx * ncy;
+  P->NT = (P->n + 7) / 8; P->QT = (nq + 7) / 8;
+  P->NP = 8 * P->NT; P->QP = 8 * P->QT;
+  P->nix = ncx * p - 1; P->niy = ncy * p - 1;
+  if (p == 1) { P->nix = ncx - 1; P->niy = ncy - 1; }
+  P->ncomp = (long long)ncx * P->n * ncy * P->n;
+  P->ndof_psi = P->ncomp * (kind == HPG_OBSTACLE ? 1 : 2);
+  P->ndof_u = (long long)P->nix * P->niy;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (P->n > 128 || nq > 256) { delete P; return fail(HPG_ERR_UNSUPPORTED, "n > 128 or nq > 256"); }
+
+  std::vector<double> sf = pk_table(S, nq, P->n, P->QT, P->NP);
+  std::vector<double> tf = pk_table(T, P->n, nq, P->NT, P->QP);
+  int rc;
+  if ((rc = upload(&P->Sf, sf.data(), sf.size()))) { delete P; return rc; }
+  if ((rc = upload(&P->Tf, tf.data(), tf.size()))) { delete P; return rc; }
+  if ((rc = upload(&P->hx, hx, ncx))) { delete P; return rc; }
+  if ((rc = upload(&P->hy, hy, ncy))) { delete P; return rc; }
+  // u side (load_vector): analysis with Tu, tile side m
+  P->NTu = (P->m + 7) / 8;
+  std::vector<double> tuf = pk_table(Tu, P->m, nq, P->NTu, P->QP);
+  std::vector<double> suf = pk_table(Su, nq, P->m, P->QT, 8 * P->NTu);
+  if ((rc = upload(&P->Tuf, tuf.data(), tuf.size()))) { delete P; return rc; }
+  if ((rc = upload(&P->Suf, suf.data(), suf.size()))) { delete P; return rc; }
+  // block table G[(a,j)][g] = T[a][g] S[g][j]
+  int n2 = P->n * P->n;
+  std::vector<double> G((size_t)n2 * P->QP, 0.0);
+  for (int a = 0; a < P->n; ++a)
+    for (int j = 0; j < P->n; ++j)
+      for (int g = 0; g < nq; ++g)
+        G[((size_t)a * P->n + j) * P->QP + g] = T[(size_t)a * nq + g] * S[(size_t)g * P->n + j];
+  if ((rc = upload(&P->G, G.data(), G.size()))) { delete P; return rc; }
+  cudaError_t e = cudaMalloc(&P->scratch_u, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
+  if (e == cudaSuccess) e = cudaMalloc(&P->mu, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
+  if (e == cudaSuccess) e = cudaMalloc(&P->dflag, sizeof(int) * 4);
+  if (e != cudaSuccess) { delete P; return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+
+  // path selection
+  P->use_warp[M_OBST_RES] = warp_fits(M_OBST_RES, P->NT, P->QT);
+  P->use_warp[M_OBST_APPLY] = warp_fits(M_OBST_APPLY, P->NT, P->QT);
+  P->use_warp[M_OBST_CACHED] = warp_fits(M_OBST_CACHED, P->NT, P->QT);
+  P->use_warp[M_GRAD_RES] = warp_fits(M_GRAD_RES, P->NT, P->QT);
+  P->use_warp[M_GRAD_APPLY] = warp_fits(M_GRAD_APPLY, P->NT, P->QT);
+  P->use_warp[M_GRAD_CACHED] = warp_fits(M_GRAD_CACHED, P->NT, P->QT);
+  P->use_warp[M_VALUES] = 0;
+  // split the Q row tiles of an element across CTAs when there are few elements
+  P->splits = 1;
+  if (P->N < 2 * P->nsm) {
+    int want = (2 * P->nsm + P->N - 1) / P->N;
+    P->splits = want < P->QT ? want : P->QT;
+    if (P->splits < 1) P->splits = 1;
+  }
+  P->partial_len = (size_t)P->N * P->splits * 2 * P->NP * P->NP;
+  int NPu = 8 * P->NTu;
+  size_t plu = (size_t)P->N * P->splits * NPu * NPu;
+  if (plu > P->partial_len) P->partial_len = plu;
+  e = cudaMalloc(&P->partial, sizeof(double) * P->partial_len + 16);
+  if (e != cudaSuccess) { delete P; return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+  *plan = P;
+  return HPG_OK;
+}
+
+int hpgPlanDestroy(hpgPlan P) {
+  if (P == nullptr) return HPG_OK;
+  cudaFree(P->Sf); cudaFree(P->Tf); cudaFree(P->hx); cudaFree(P->hy); cudaFree(P->G);
+  cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
+  cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag);
+  delete P;
+  return HPG_OK;
+}
+
+int hpgPlanInfo(hpgPlan P, long long* info) {
+  if (int rc = check(P)) return rc;
+  int nw = P->kind == HPG_OBSTACLE ? 1 : 3;
+  info[0] = P->n;
+  info[1] = P->m;
+  info[2] = P->nq;
+  info[3] = P->N;
+  info[4] = P->ndof_psi;
+  info[5] = P->ndof_u;
+  info[6] = (long long)P->N * P->QT * P->QT * nw * 64;
+  long long nb = (long long)P->n * P->n * (P->kind == HPG_OBSTACLE ? 1 : 2);
+  info[7] = nb * nb;
+  info[8] = P->kind == HPG_OBSTACLE ? (P->use_warp[M_OBST_RES] ? 0 : 1) : (P->use_warp[M_GRAD_RES] ? 0 : 1);
+  info[9] = P->splits;
+  return HPG_OK;
+}
+
+int hpgObstacleMoments(hpgPlan P, const double* psi, double* out, int* clamped, double* wcache, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (P->kind != HPG_OBSTACLE) return fail(HPG_ERR_ARG, "plan is not an obstacle plan");
+  if (!psi || !out || !clamped) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.in0 = psi; A.out = out; A.flag = clamped; A.wc_out = wcache;
+  return run_elem<M_OBST_RES>(P, A, (cudaStream_t)stream);
+}
+
+int hpgObstacleApplyD(hpgPlan P, const double* psi, const double* x, double* y, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (P->kind != HPG_OBSTACLE) return fail(HPG_ERR_ARG, "plan is not an obstacle plan");
+  if (!psi || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.in0 = psi; A.in1 = x; A.out = y;
+  return run_elem<M_OBST_APPLY>(P, A, (cudaStream_t)stream);
+}
+
+int hpgGradientMoments(hpgPlan P, const double* psi, const double* phi, double* out, double* wcache, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (P->kind != HPG_GRADIENT) return fail(HPG_ERR_ARG, "plan is not a gradient plan");
+  if (!psi || !phi || !out) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.in0 = psi; A.phi = phi; A.out = out; A.wc_out = wcache; A.flag = P->dflag;
+  return run_elem<M_GRAD_RES>(P, A, (cudaStream_t)stream);
+}
+
+int hpgGradientApplyD(hpgPlan P, const double* psi, const double* phi, const double* x, double* y, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (P->kind != HPG_GRADIENT) return fail(HPG_ERR_ARG, "plan is not a gradient plan");
+  if (!psi || !phi || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.in0 = psi; A.in1 = x; A.phi = phi; A.out = y;
+  return run_elem<M_GRAD_APPLY>(P, A, (cudaStream_t)stream);
+}
+
+int hpgApplyCached(hpgPlan P, const double* wcache, const double* x, double* y, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.wc_in = wcache; A.in1 = x; A.out = y;
+  if (P->kind == HPG_OBSTACLE) return run_elem<M_OBST_CACHED>(P, A, (cudaStream_t)stream);
+  return run_elem<M_GRAD_CACHED>(P, A, (cudaStream_t)stream);
+}
+
+int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u, const double* psi,
+                const double* phi, const double* f_load, double* b_u, double* b_psi, int* clamped,
+                double* wcache, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!psi_prev || !u || !psi || !phi || !f_load || !b_u || !b_psi) return fail(HPG_ERR_ARG, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  ElemArgs A = base_args(P);
+  A.in0 = psi; A.out = b_psi; A.wc_out = wcache; A.residual = 1; A.u = u;
+  int rc;
+  if (P->kind == HPG_OBSTACLE) {
+    if (!clamped) return fail(HPG_ERR_ARG, "null clamp flag");
+    A.phi_mom = phi; A.flag = clamped;
+    rc = run_elem<M_OBST_RES>(P, A, s);
+  } else {
+    A.phi = phi; A.flag = P->dflag;
+    rc = run_elem<M_GRAD_RES>(P, A, s);
+  }
+  if (rc) return rc;
+  UArgs U = base_uargs(P);
+  U.u = u; U.ca = -alpha; U.psi_a = psi_prev; U.psi_b = psi;
+  U.base = f_load; U.cbase = alpha; U.out = b_u;
+  return run_ulocal(P, U, s);
+}
+
+int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!wcache || !blocks) return fail(HPG_ERR_ARG, "null pointer");
+  if (c0 < 0 || count < 0 || c0 + count > P->N) return fail(HPG_ERR_ARG, "cell range out of bounds");
+  if (count == 0) return HPG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int nf = P->kind == HPG_OBSTACLE ? 1 : 3;
+  int n2 = P->n * P->n;
+  // stage-1 scratch sized for up to 256 MB of Z per pass
+  size_t per_cell = (size_t)nf * n2 * P->QP;
+  int chunk = (int)((256ull << 20) / (sizeof(double) * per_cell));
+  if (chunk < 1) chunk = 1;
+  if (chunk > P->N) chunk = P->N;
+  if (P->Z == nullptr || P->zcells < chunk) {
+    cudaFree(P->Z);
+    P->Z = nullptr;
+    CUDA_TRY(cudaMalloc(&P->Z, sizeof(double) * per_cell * chunk + 16));
+    P->zcells = chunk;
+  }
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.nfield = nf; g.n = P->n; g.n2 = n2; g.QP = P->QP; g.QT = P->QT; g.NW = nf;
+  g.ncy = P->ncy; g.G = P->G; g.wc = wcache; g.Z = P->Z;
+  g.nb = (long long)n2 * (P->kind == HPG_OBSTACLE ? 1 : 2);
+  g.hx = P->hx; g.hy = P->hy;
+  for (int start = c0; start < c0 + count; start += P->zcells) {
+    int cnt = c0 + count - start < P->zcells ? c0 + count - start : P->zcells;
+    g.cell0 = start;
+    g.out = blocks + (size_t)(start - c0) * g.nb * g.nb;
+    g.M = n2; g.N = P->QP; g.K = P->QP;
+    dim3 g1((n2 + GT - 1) / GT, (P->QP + GT - 1) / GT, cnt * nf);
+    k_gemm<0><<<g1, 256, 0, s>>>(g);
+    LAUNCH_CHECK();
+    g.M = n2; g.N = n2; g.K = P->QP;
+    dim3 g2((n2 + GT - 1) / GT, (n2 + GT - 1) / GT, cnt * nf);
+    k_gemm<1><<<g2, 256, 0, s>>>(g);
+    LAUNCH_CHECK();
+  }
+  return HPG_OK;
+}
+
+int hpgBlocksMatvec(hpgPlan P, const double* blocks, const double* x, double* y, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!blocks || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  int nb = P->n * P->n * (P->kind == HPG_OBSTACLE ? 1 : 2);
+  size_t smem = sizeof(double) * nb;
+  if (smem > 48 * 1024) {
+    CUDA_TRY(cudaFuncSetAttribute(k_blocks_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  k_blocks_matvec<<<P->N, 256, smem, (cudaStream_t)stream>>>(A, blocks, nb, 0, x, y);
+  LAUNCH_CHECK();
+  return HPG_OK;
+}
+
+int hpgBTu(hpgPlan P, const double* u, double* out, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!u || !out) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.u = u; A.out = out;
+  long long total = P->ndof_psi;
+  k_btu<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(A, P->kind == HPG_GRADIENT);
+  LAUNCH_CHECK();
+  return HPG_OK;
+}
+
+int hpgBPsi(hpgPlan P, const double* psi, double* out, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!psi || !out) return fail(HPG_ERR_ARG, "null pointer");
+  UArgs U = base_uargs(P);
+  U.psi_a = psi; U.out = out;
+  return run_ulocal(P, U, (cudaStream_t)stream);
+}
+
+int hpgAu(hpgPlan P, const double* u, double* out, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!u || !out) return fail(HPG_ERR_ARG, "null pointer");
+  UArgs U = base_uargs(P);
+  U.u = u; U.ca = 1.0; U.out = out;
+  return run_ulocal(P, U, (cudaStream_t)stream);
+}
+
+int hpgMomentsFromValues(hpgPlan P, const double* vals, double* out, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!vals || !out) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs A = base_args(P);
+  A.in0 = vals; A.out = out;
+  A.splits = P->splits;
+  return run_mode<M_VALUES>(false, A, (cudaStream_t)stream);
+}
+
+int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!vals || !out) return fail(HPG_ERR_ARG, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  // U-side moments Mu = wu (x) wu * (Tu F Tu^T) as x-major m-tiles
+  ElemArgs A = base_args(P);
+  A.n = P->m; A.NT = P->NTu; A.Tf = P->Tuf; A.Sf = P->Suf;
+  A.ld = (long long)P->ncy * P->m;
+  A.ncomp = (long long)P->ncx * P->m * P->ncy * P->m;
+  A.in0 = vals; A.out = P->mu;
+  A.splits = P->splits;
+  int rc = run_mode<M_VALUES>(false, A, s);
+  if (rc) return rc;
+  UArgs U = base_uargs(P);
+  U.mu = P->mu; U.out = out;
+  return run_ulocal(P, U, s);
+}
+
+}  // extern "C"

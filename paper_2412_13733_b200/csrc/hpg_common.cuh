@@ -1,0 +1,148 @@
+// Shared device helpers for the hpG element-quadrature kernels (sm_100a, fp64).
+//
+// FP64 tensor-core path on Blackwell: tcgen05.mma has no f64 kind, so the
+// FP64 tensor cores are reached through mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4,
+// measured 37.2 TF/s on this pool's B200: profiles/fp64_peaks_r01.json).
+//
+// Fragment layouts of m8n8k4 (lane = r*4 + c, r = lane>>2, c = lane&3):
+//   A (8x4):  A[r][c]            B (4x8):  B[c][r]
+//   C/D (8x8): C[r][2c], C[r][2c+1]
+// "Permuted K" trick used throughout: a C fragment of an 8x8 tile is directly
+// the A fragment (rows r) -- and, transposed, the B fragment (cols r) -- of
+// the next contraction if that contraction's K index runs over the tile's
+// columns in the order {0,2,4,6} (k-step 2t) then {1,3,5,7} (k-step 2t+1).
+// The other operand of such a contraction is a table read in the matching
+// permuted order: PK(X)[tile][ks][lane] = X[8*tile + r][8*(ks>>1) + 2c + (ks&1)].
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hpg {
+
+constexpr double EXP_CLAMP = 700.0;   // hpgalerkin/assembly.py:25
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+// exp(min(-v, 700)) with the reference's overflow flag (assembly.py:187-192):
+// flagged iff -v > 700 or v is NaN; underflow to 0 is legitimate.  A select,
+// not fmin: fmin(NaN, 700) would return 700 where the reference keeps NaN.
+__device__ __forceinline__ double clamped_exp_neg(double v, bool& flag) {
+  double t = -v;
+  bool over = t > EXP_CLAMP;
+  flag |= over || (v != v);
+  return exp(over ? EXP_CLAMP : t);
+}
+
+// ---------------------------------------------------------------------------
+// Per-launch arguments (plain pointers; no torch types).
+struct ElemArgs {
+  int ncx, ncy, n, m, p, nq, N;
+  int nix, niy;
+  long long ld;      // row stride of the x-major psi array (= ncy*n)
+  long long ncomp;   // psi dofs per component
+  const double* hx;
+  const double* hy;
+  const double* Sf;  // PK(S): [QT][NP/4][32]
+  const double* Tf;  // PK(T): [NT][QP/4][32]
+  const double* in0; // psi (or values for M_VALUES)
+  const double* in1; // direction x
+  const double* phi; // gradient point samples, (N, nq, nq)
+  const double* wc_in;
+  double* wc_out;
+  double* out;
+  int* flag;
+  int residual;      // 1: out = phi_mom - B^T u - M (obstacle) | M - B^T u (gradient)
+  const double* phi_mom;
+  const double* u;
+  // generic (CTA) path only
+  int NT, QT, splits;
+  double* partial;   // [N][splits][NOUT][NP*NP] when splits > 1
+  int out_cellmajor; // M_VALUES for the u side: out is (N, n, n) cell-major
+};
+
+enum Mode : int {
+  M_OBST_RES = 0,     // psi -> exp moments (+ weight cache, flag)
+  M_OBST_APPLY = 1,   // psi, x -> D x   (weights recomputed)
+  M_OBST_CACHED = 2,  // cache, x -> D x
+  M_GRAD_RES = 3,     // psi_x, psi_y, phi -> nl moments (+ cache: kxx, kxy, kyy)
+  M_GRAD_APPLY = 4,   // psi, x, phi -> D x
+  M_GRAD_CACHED = 5,  // cache, x -> D x
+  M_VALUES = 6,       // point values -> moments (data_moments, load_vector)
+};
+
+template <int MODE> struct ModeTraits;
+template <> struct ModeTraits<M_OBST_RES>    { static constexpr int NIN = 1, NSYN = 1, NOUT = 1, NW = 1; };
+template <> struct ModeTraits<M_OBST_APPLY>  { static constexpr int NIN = 2, NSYN = 2, NOUT = 1, NW = 1; };
+template <> struct ModeTraits<M_OBST_CACHED> { static constexpr int NIN = 1, NSYN = 1, NOUT = 1, NW = 1; };
+template <> struct ModeTraits<M_GRAD_RES>    { static constexpr int NIN = 2, NSYN = 2, NOUT = 2, NW = 3; };
+template <> struct ModeTraits<M_GRAD_APPLY>  { static constexpr int NIN = 4, NSYN = 4, NOUT = 2, NW = 3; };
+template <> struct ModeTraits<M_GRAD_CACHED> { static constexpr int NIN = 2, NSYN = 2, NOUT = 2, NW = 3; };
+template <> struct ModeTraits<M_VALUES>      { static constexpr int NIN = 0, NSYN = 0, NOUT = 1, NW = 0; };
+
+// Global address of psi-side tile entry (a, b) of cell (cx, cy), component f.
+__device__ __forceinline__ long long psi_index(const ElemArgs& A, int cx, int cy, int a, int b) {
+  return (long long)(cx * A.n + a) * A.ld + (long long)cy * A.n + b;
+}
+
+// Interior index of cell-local U dof j in 1D (-1 on the boundary).
+// Local order [hat_L, hat_R, W_0..W_{p-2}] (spaces.py:40-43); the 1D interior
+// numbering is hats 1..nc-1 then bubbles cell by cell (spaces.py:25-38).
+__device__ __forceinline__ int u_local_1d(int c, int j, int nc, int p) {
+  if (j == 0) return c >= 1 ? c - 1 : -1;
+  if (j == 1) return c + 1 <= nc - 1 ? c : -1;
+  return (nc - 1) + c * (p - 1) + (j - 2);
+}
+
+__device__ __forceinline__ double u_at(const ElemArgs& A, int cx, int cy, int i, int j) {
+  int ix = u_local_1d(cx, i, A.ncx, A.p);
+  int iy = u_local_1d(cy, j, A.ncy, A.p);
+  if (ix < 0 || iy < 0) return 0.0;
+  return __ldg(A.u + (long long)ix * A.niy + iy);
+}
+
+// Row a of the U->Legendre map R (spaces.py:45-57): up to 3 (col, coef).
+__device__ __forceinline__ int legendre_row(int a, int p, int* col, double* coef) {
+  int k = 0;
+  if (a == 0) { col[k] = 0; coef[k++] = 0.5; col[k] = 1; coef[k++] = 0.5; }
+  if (a == 1) { col[k] = 0; coef[k++] = -0.5; col[k] = 1; coef[k++] = 0.5; }
+  if (a <= p - 2) { col[k] = 2 + a; coef[k++] = 1.0 / (2 * a + 3); }
+  if (a >= 2 && a - 2 <= p - 2) { col[k] = a; coef[k++] = -1.0 / (2 * a - 1); }
+  return k;
+}
+
+// Row i of the derivative map D (spaces.py:59-68).
+__device__ __forceinline__ int deriv_row(int i, int p, int* col, double* coef) {
+  int k = 0;
+  if (i == 0) { col[k] = 0; coef[k++] = -0.5; col[k] = 1; coef[k++] = 0.5; }
+  if (i >= 1 && i - 1 <= p - 2) { col[k] = 2 + (i - 1); coef[k++] = -1.0; }
+  return k;
+}
+
+// (B^T u) at psi-tile entry (a, b) of cell (cx, cy), component comp
+// (assembly.py:81-116,475-477,725-729):
+//   obstacle:  wx_a wy_b (Rx C Ry^T)[a][b]
+//   gradient x: (2/(2a+1)) (Dx C Ry^T)[a][b] wy_b ; y: wx_a (Rx C Dy^T)[a][b] (2/(2b+1))
+__device__ __forceinline__ double btu_value(const ElemArgs& A, bool gradient, int comp,
+                                            int cx, int cy, int a, int b,
+                                            double wa, double wb) {
+  int ci[3], cj[3];
+  double ai[3], aj[3];
+  int ni, nj;
+  if (gradient && comp == 0) ni = deriv_row(a, A.p, ci, ai); else ni = legendre_row(a, A.p, ci, ai);
+  if (gradient && comp == 1) nj = deriv_row(b, A.p, cj, aj); else nj = legendre_row(b, A.p, cj, aj);
+  double s = 0.0;
+  for (int x = 0; x < ni; ++x) {
+    double t = 0.0;
+    for (int y = 0; y < nj; ++y) t += aj[y] * u_at(A, cx, cy, ci[x], cj[y]);
+    s += ai[x] * t;
+  }
+  double fa = wa, fb = wb;
+  if (gradient && comp == 0) fa = 2.0 / (2 * a + 1);
+  if (gradient && comp == 1) fb = 2.0 / (2 * b + 1);
+  return (fa * s) * fb;
+}
+
+}  // namespace hpg

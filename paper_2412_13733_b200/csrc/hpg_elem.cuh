@@ -1,0 +1,386 @@
+// Stage (a)->(b)->(c) element kernels: sum-factorised synthesis, pointwise
+// LVPP map and test-side analysis, fused so point values never touch HBM.
+//
+// Per element (tile side n padded to NP = 8*NT, Q padded to QP = 8*QT), for
+// each 8-row tile rt of the Q x Q point grid:
+//   P_rt  = S[rt,:] C            (8 x NP)   A = PK(S) (smem), B = C (smem)
+//   V_rt  = P_rt S^T             (8 x QP)   A = P (regs),     B = PK(S)
+//   W_rt  = map(V_rt, ...)                  pointwise, in registers
+//   R_rt  = T W_rt^T             (NP x 8)   A = PK(T),        B = W (regs)
+//   Y    += R_rt T[:,rt]^T       (NP x NP)  A = R (regs),     B = PK(T)
+// and M[a][b] = w_a w_b Y[b][a] (reference CellKernel2D.moments,
+// assembly.py:249-251).  Zero-padded tables make the padded rows/cols inert.
+#pragma once
+#include "hpg_common.cuh"
+#include "hpg_pointmap.cuh"
+
+namespace hpg {
+
+constexpr int WARP_CTA_WARPS = 4;
+constexpr int CTA_WARPS = 8;
+
+template <int MODE>
+__device__ __forceinline__ void field_src(const ElemArgs& A, int f, const double*& ptr, int& comp) {
+  if constexpr (MODE == M_OBST_RES) { ptr = A.in0; comp = 0; }
+  else if constexpr (MODE == M_OBST_APPLY) { ptr = f == 0 ? A.in0 : A.in1; comp = 0; }
+  else if constexpr (MODE == M_OBST_CACHED) { ptr = A.in1; comp = 0; }
+  else if constexpr (MODE == M_GRAD_RES) { ptr = A.in0; comp = f; }
+  else if constexpr (MODE == M_GRAD_APPLY) { ptr = f < 2 ? A.in0 : A.in1; comp = f & 1; }
+  else if constexpr (MODE == M_GRAD_CACHED) { ptr = A.in1; comp = f; }
+  else { ptr = nullptr; comp = 0; }
+}
+
+__device__ __forceinline__ long long wc_index(int e, int QT, int rt, int ht, int NW, int w, int lane) {
+  return (((((long long)e * QT + rt) * QT + ht) * NW + w) * 32 + lane) * 2;
+}
+
+// Final value of moment (a, b), output component o, of cell e.
+template <int MODE>
+__device__ __forceinline__ void write_moment(const ElemArgs& A, int e, int cx, int cy, int o,
+                                             int a, int b, double y) {
+  constexpr bool gradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
+  double wa = A.hx[cx] / (2.0 * a + 1.0);
+  double wb = A.hy[cy] / (2.0 * b + 1.0);
+  double val = (wa * y) * wb;
+  if (A.out_cellmajor) {
+    A.out[((long long)e * A.n + a) * A.n + b] = val;
+    return;
+  }
+  long long idx = (long long)o * A.ncomp + psi_index(A, cx, cy, a, b);
+  if (A.residual) {
+    // proximal.py:123 / :125
+    double btu = btu_value(A, gradient, o, cx, cy, a, b, wa, wb);
+    if constexpr (gradient) val = val - btu;
+    else val = (__ldg(A.phi_mom + idx) - btu) - val;
+  }
+  A.out[idx] = val;
+}
+
+// Stage (b) for one C-fragment position pair (j = 0, 1) of tile (rt, ht).
+template <int MODE, int NSYN, int NOUT, int NW>
+__device__ __forceinline__ void map_pair(const ElemArgs& A, int e, int QT, int rt, int ht, int lane,
+                                         const double (&V)[NSYN > 0 ? NSYN : 1][2],
+                                         double (&Vw)[NOUT][2], bool& flag) {
+  constexpr bool gradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
+  constexpr bool cached = MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED;
+  constexpr bool writes = MODE == M_OBST_RES || MODE == M_GRAD_RES;
+  const int r = lane >> 2, c = lane & 3;
+  const int g = 8 * rt + r;
+  double win[NW > 0 ? NW : 1][2], wout[NW > 0 ? NW : 1][2];
+  if constexpr (cached) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      double2 t = __ldg(reinterpret_cast<const double2*>(A.wc_in + wc_index(e, QT, rt, ht, NW, w, lane)));
+      win[w][0] = t.x;
+      win[w][1] = t.y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int h = 8 * ht + 2 * c + j;
+    const bool inside = g < A.nq && h < A.nq;
+    double v[NSYN > 0 ? NSYN : 1];
+    double vw[NOUT];
+    double wi[NW > 0 ? NW : 1], wo[NW > 0 ? NW : 1];
+    if constexpr (MODE == M_VALUES) {
+      vw[0] = inside ? __ldg(A.in0 + ((long long)e * A.nq + g) * A.nq + h) : 0.0;
+    } else {
+#pragma unroll
+      for (int f = 0; f < NSYN; ++f) v[f] = V[f][j];
+      double phi = 0.0;
+      if constexpr (gradient) {
+        if (!cached && inside) phi = __ldg(A.phi + ((long long)e * A.nq + g) * A.nq + h);
+      }
+#pragma unroll
+      for (int w = 0; w < NW; ++w) wi[w] = win[w][j];
+      bool fl = false;
+      point_map<MODE>(v, phi, wi, wo, vw, fl);
+      // padded points (g or h >= nq) are inert: zero weight, never flagged
+      // (0 * inf in the padded table rows must not leak NaN into the cell)
+      if (inside) {
+        flag |= fl;
+      } else {
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) vw[o] = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) wo[w] = 0.0;
+      }
+#pragma unroll
+      for (int w = 0; w < NW; ++w) wout[w][j] = wo[w];
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) Vw[o][j] = vw[o];
+  }
+  if constexpr (writes) {
+    if (A.wc_out != nullptr) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        *reinterpret_cast<double2*>(A.wc_out + wc_index(e, QT, rt, ht, NW, w, lane)) =
+            make_double2(wout[w][0], wout[w][1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-per-element kernel: all fragments in registers, tables in smem.
+template <int NT, int QT, int MODE>
+__global__ void __launch_bounds__(32 * WARP_CTA_WARPS)
+k_warp(ElemArgs A) {
+  using TR = ModeTraits<MODE>;
+  constexpr int NP = 8 * NT, QP = 8 * QT, NK = NP / 4, QK = QP / 4;
+  constexpr int LDT = NP + 2, TILE = NP * LDT;
+  constexpr int NIN = TR::NIN, NSYN = TR::NSYN, NOUT = TR::NOUT, NW = TR::NW;
+  extern __shared__ double smem[];
+  double* sS = smem;
+  double* sT = sS + QP * NP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, c = lane & 3;
+  double* sTile = sT + NP * QP + warp * (NIN > 0 ? NIN * TILE : 0);
+  for (int i = threadIdx.x; i < QP * NP; i += blockDim.x) {
+    sS[i] = A.Sf[i];
+    sT[i] = A.Tf[i];
+  }
+  __syncthreads();
+
+  for (int e = blockIdx.x * WARP_CTA_WARPS + warp; e < A.N; e += gridDim.x * WARP_CTA_WARPS) {
+    const int cx = e / A.ncy, cy = e - cx * A.ncy;
+#pragma unroll
+    for (int f = 0; f < NIN; ++f) {
+      const double* src;
+      int comp;
+      field_src<MODE>(A, f, src, comp);
+      src += comp * A.ncomp;
+      for (int idx = lane; idx < NP * NP; idx += 32) {
+        int a = idx / NP, b = idx - a * NP;
+        double v = 0.0;
+        if (a < A.n && b < A.n) v = __ldg(src + psi_index(A, cx, cy, a, b));
+        sTile[f * TILE + a * LDT + b] = v;
+      }
+    }
+    __syncwarp();
+
+    double Y[NOUT][NT][NT][2];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int k = 0; k < NT; ++k) Y[o][i][k][0] = Y[o][i][k][1] = 0.0;
+    bool flag = false;
+
+#pragma unroll 1
+    for (int rt = 0; rt < QT; ++rt) {
+      double V[NSYN > 0 ? NSYN : 1][QT][2];
+#pragma unroll
+      for (int f = 0; f < NSYN; ++f) {
+        double P[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) P[nt][0] = P[nt][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < NK; ++ks) {
+          double a = sS[(rt * NK + ks) * 32 + lane];
+          const double* row = sTile + f * TILE + (8 * (ks >> 1) + 2 * c + (ks & 1)) * LDT + r;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma(P[nt], a, row[8 * nt]);
+        }
+#pragma unroll
+        for (int ht = 0; ht < QT; ++ht) {
+          V[f][ht][0] = V[f][ht][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < NK; ++ks)
+            dmma(V[f][ht], P[ks >> 1][ks & 1], sS[(ht * NK + ks) * 32 + lane]);
+        }
+      }
+      double Vw[NOUT][QT][2];
+#pragma unroll
+      for (int ht = 0; ht < QT; ++ht) {
+        double Vp[NSYN > 0 ? NSYN : 1][2];
+#pragma unroll
+        for (int f = 0; f < NSYN; ++f) { Vp[f][0] = V[f][ht][0]; Vp[f][1] = V[f][ht][1]; }
+        double out2[NOUT][2];
+        map_pair<MODE, NSYN, NOUT, NW>(A, e, QT, rt, ht, lane, Vp, out2, flag);
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) { Vw[o][ht][0] = out2[o][0]; Vw[o][ht][1] = out2[o][1]; }
+      }
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        double R[NT][2];
+#pragma unroll
+        for (int bt = 0; bt < NT; ++bt) {
+          R[bt][0] = R[bt][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < QK; ++ks)
+            dmma(R[bt], sT[(bt * QK + ks) * 32 + lane], Vw[o][ks >> 1][ks & 1]);
+        }
+#pragma unroll
+        for (int bt = 0; bt < NT; ++bt)
+#pragma unroll
+          for (int at = 0; at < NT; ++at)
+#pragma unroll
+            for (int k2 = 0; k2 < 2; ++k2)
+              dmma(Y[o][bt][at], R[bt][k2], sT[(at * QK + 2 * rt + k2) * 32 + lane]);
+      }
+    }
+    if constexpr (MODE == M_OBST_RES) {
+      if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+      for (int bt = 0; bt < NT; ++bt)
+#pragma unroll
+        for (int at = 0; at < NT; ++at)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            int a = 8 * at + 2 * c + j, b = 8 * bt + r;
+            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j]);
+          }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-per-(element, row-tile range) kernel for any size (runtime NT, QT):
+// the same four contractions, warps splitting tiles, stage results passed
+// through shared memory in C-fragment order (read back with LDS.128 by the
+// same lane).  Used for large n (config 3) and as the general path.
+template <int MODE, int MAXS>
+__global__ void __launch_bounds__(32 * CTA_WARPS, 1)
+k_cta(ElemArgs A) {
+  using TR = ModeTraits<MODE>;
+  constexpr int NIN = TR::NIN, NSYN = TR::NSYN, NOUT = TR::NOUT, NW = TR::NW;
+  const int NT = A.NT, QT = A.QT;
+  const int NP = 8 * NT, NK = NP / 4, QK = 2 * QT;
+  const int LDT = NP + 2, TILE = NP * LDT;
+  extern __shared__ double smem[];
+  double* sTile = smem;
+  double* sP = sTile + NIN * TILE;               // [NSYN][NT][64]
+  double* sV = sP + NSYN * NT * 64;               // [NOUT][QT][64]
+  double* sR = sV + NOUT * QT * 64;               // [NOUT][NT][64]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, c = lane & 3;
+  const int e = blockIdx.x / A.splits, sp = blockIdx.x - e * A.splits;
+  if (e >= A.N) return;
+  const int rt0 = (sp * QT) / A.splits, rt1 = ((sp + 1) * QT) / A.splits;
+  const int cx = e / A.ncy, cy = e - cx * A.ncy;
+
+  for (int f = 0; f < NIN; ++f) {
+    const double* src;
+    int comp;
+    field_src<MODE>(A, f, src, comp);
+    src += comp * A.ncomp;
+    for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
+      int a = idx / NP, b = idx - a * NP;
+      double v = 0.0;
+      if (a < A.n && b < A.n) v = __ldg(src + psi_index(A, cx, cy, a, b));
+      sTile[f * TILE + a * LDT + b] = v;
+    }
+  }
+  __syncthreads();
+
+  const int ny = NOUT * NT * NT;
+  double Y[MAXS][2];
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s) Y[s][0] = Y[s][1] = 0.0;
+  bool flag = false;
+
+  for (int rt = rt0; rt < rt1; ++rt) {
+    // (1) P tiles
+    for (int it = warp; it < NSYN * NT; it += CTA_WARPS) {
+      int f = it / NT, nt = it - f * NT;
+      double P[2] = {0.0, 0.0};
+      const double* col = sTile + f * TILE + 8 * nt + r;
+      for (int ks = 0; ks < NK; ++ks)
+        dmma(P, __ldg(A.Sf + (rt * NK + ks) * 32 + lane), col[(8 * (ks >> 1) + 2 * c + (ks & 1)) * LDT]);
+      *reinterpret_cast<double2*>(sP + (f * NT + nt) * 64 + 2 * lane) = make_double2(P[0], P[1]);
+    }
+    __syncthreads();
+    // (2) V tiles + pointwise map
+    for (int ht = warp; ht < QT; ht += CTA_WARPS) {
+      double V[NSYN > 0 ? NSYN : 1][2];
+#pragma unroll
+      for (int f = 0; f < NSYN; ++f) {
+        V[f][0] = V[f][1] = 0.0;
+        for (int t = 0; t < NT; ++t) {
+          double2 pa = *reinterpret_cast<const double2*>(sP + (f * NT + t) * 64 + 2 * lane);
+          dmma(V[f], pa.x, __ldg(A.Sf + (ht * NK + 2 * t) * 32 + lane));
+          dmma(V[f], pa.y, __ldg(A.Sf + (ht * NK + 2 * t + 1) * 32 + lane));
+        }
+      }
+      double out2[NOUT][2];
+      map_pair<MODE, NSYN, NOUT, NW>(A, e, QT, rt, ht, lane, V, out2, flag);
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o)
+        *reinterpret_cast<double2*>(sV + (o * QT + ht) * 64 + 2 * lane) = make_double2(out2[o][0], out2[o][1]);
+    }
+    __syncthreads();
+    // (3) R tiles
+    for (int it = warp; it < NOUT * NT; it += CTA_WARPS) {
+      int o = it / NT, bt = it - o * NT;
+      double R[2] = {0.0, 0.0};
+      for (int t = 0; t < QT; ++t) {
+        double2 vb = *reinterpret_cast<const double2*>(sV + (o * QT + t) * 64 + 2 * lane);
+        dmma(R, __ldg(A.Tf + (bt * QK + 2 * t) * 32 + lane), vb.x);
+        dmma(R, __ldg(A.Tf + (bt * QK + 2 * t + 1) * 32 + lane), vb.y);
+      }
+      *reinterpret_cast<double2*>(sR + (o * NT + bt) * 64 + 2 * lane) = make_double2(R[0], R[1]);
+    }
+    __syncthreads();
+    // (4) Y accumulation (tiles statically owned by warps)
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) {
+      int it = warp + CTA_WARPS * s;
+      if (it < ny) {
+        int o = it / (NT * NT), rem = it - o * NT * NT;
+        int bt = rem / NT, at = rem - bt * NT;
+        double2 ra = *reinterpret_cast<const double2*>(sR + (o * NT + bt) * 64 + 2 * lane);
+        dmma(Y[s], ra.x, __ldg(A.Tf + (at * QK + 2 * rt) * 32 + lane));
+        dmma(Y[s], ra.y, __ldg(A.Tf + (at * QK + 2 * rt + 1) * 32 + lane));
+      }
+    }
+  }
+  if constexpr (MODE == M_OBST_RES) {
+    if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
+  }
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s) {
+    int it = warp + CTA_WARPS * s;
+    if (it < ny) {
+      int o = it / (NT * NT), rem = it - o * NT * NT;
+      int bt = rem / NT, at = rem - bt * NT;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        int a = 8 * at + 2 * c + j, b = 8 * bt + r;
+        if (A.splits == 1) {
+          if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[s][j]);
+        } else {
+          A.partial[(((long long)e * A.splits + sp) * NOUT + o) * NP * NP + a * NP + b] = Y[s][j];
+        }
+      }
+    }
+  }
+}
+
+// Deterministic reduction of the row-tile-split partials + epilogue.
+template <int MODE>
+__global__ void k_cta_reduce(ElemArgs A) {
+  using TR = ModeTraits<MODE>;
+  constexpr int NOUT = TR::NOUT;
+  const int NP = 8 * A.NT;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)A.N * NOUT * A.n * A.n;
+  if (tid >= total) return;
+  int b = tid % A.n;
+  long long t = tid / A.n;
+  int a = t % A.n;
+  t /= A.n;
+  int o = t % NOUT;
+  int e = (int)(t / NOUT);
+  double y = 0.0;
+  for (int sp = 0; sp < A.splits; ++sp)
+    y += A.partial[(((long long)e * A.splits + sp) * NOUT + o) * NP * NP + a * NP + b];
+  const int cx = e / A.ncy, cy = e - cx * A.ncy;
+  write_moment<MODE>(A, e, cx, cy, o, a, b, y);
+}
+
+}  // namespace hpg

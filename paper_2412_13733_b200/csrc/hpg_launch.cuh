@@ -1,0 +1,19 @@
+// Launchers of the element kernels, one translation unit per mode
+// (hpg_mode_*.cu) so the template instantiations compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+#include "hpg_common.cuh"
+#include "../../include/hpg_b200.h"
+
+namespace hpg {
+
+int set_error(int code, const char* where, cudaError_t e);
+int set_error_msg(int code, const char* msg);
+
+// Is there a warp-per-element instantiation for (NT, QT) in this mode?
+template <int MODE> bool warp_available(int NT, int QT);
+// Launch the element kernel of MODE (warp path if use_warp, else CTA path
+// with A.splits row-tile splits + deterministic reduction).
+template <int MODE> int run_mode(bool use_warp, ElemArgs A, cudaStream_t s);
+
+}  // namespace hpg

@@ -1,0 +1,82 @@
+// Instantiation body shared by the hpg_mode_*.cu translation units.
+// Define HPG_MODE and the warp (NT, QT) list (HPG_WARP_LIST) before including.
+#pragma once
+#include "hpg_elem.cuh"
+#include "hpg_launch.cuh"
+
+namespace hpg {
+namespace {
+
+template <int NT, int QT, int MODE>
+int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
+  using TR = ModeTraits<MODE>;
+  constexpr int NP = 8 * NT, QP = 8 * QT;
+  constexpr size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * TR::NIN * NP * (NP + 2));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_warp<NT, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_warp)", e);
+    attr = true;
+  }
+  int grid = (A.N + WARP_CTA_WARPS - 1) / WARP_CTA_WARPS;
+  k_warp<NT, QT, MODE><<<grid, 32 * WARP_CTA_WARPS, smem, s>>>(A);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_warp launch", e);
+}
+
+template <int MODE, int MAXS>
+int launch_cta_t(ElemArgs A, cudaStream_t s) {
+  using TR = ModeTraits<MODE>;
+  const int NP = 8 * A.NT;
+  size_t smem = sizeof(double) * ((size_t)TR::NIN * NP * (NP + 2) +
+                                  (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64);
+  if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "element tile too large for shared memory");
+  static int attr = 0;
+  if ((int)smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_cta<MODE, MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_cta)", e);
+    attr = (int)smem;
+  }
+  k_cta<MODE, MAXS><<<A.N * A.splits, 32 * CTA_WARPS, smem, s>>>(A);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_cta launch", e);
+  if (A.splits > 1) {
+    long long total = (long long)A.N * TR::NOUT * A.n * A.n;
+    k_cta_reduce<MODE><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(A);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_cta_reduce launch", e);
+  }
+  return 0;
+}
+
+template <int MODE>
+int launch_cta(ElemArgs A, cudaStream_t s) {
+  using TR = ModeTraits<MODE>;
+  int slots = (TR::NOUT * A.NT * A.NT + CTA_WARPS - 1) / CTA_WARPS;
+  if (slots <= 4) return launch_cta_t<MODE, 4>(A, s);
+  if (slots <= 16) return launch_cta_t<MODE, 16>(A, s);
+  if (slots <= 32) return launch_cta_t<MODE, 32>(A, s);
+  return set_error_msg(HPG_ERR_UNSUPPORTED, "tile side too large");
+}
+
+}  // namespace
+
+#define HPG_W(NT_, QT_) \
+  if (NT == NT_ && QT == QT_) return launch ? launch_warp_t<NT_, QT_, HPG_MODE>(A, s) : 1;
+
+static int warp_dispatch(int NT, int QT, bool launch, const ElemArgs& A, cudaStream_t s) {
+  HPG_WARP_LIST
+  return launch ? set_error_msg(HPG_ERR_UNSUPPORTED, "no warp instantiation") : 0;
+}
+
+template <> bool warp_available<HPG_MODE>(int NT, int QT) {
+  ElemArgs dummy{};
+  return warp_dispatch(NT, QT, false, dummy, 0) == 1;
+}
+
+template <> int run_mode<HPG_MODE>(bool use_warp, ElemArgs A, cudaStream_t s) {
+  if (use_warp) return warp_dispatch(A.NT, A.QT, true, A, s);
+  return launch_cta<HPG_MODE>(A, s);
+}
+
+}  // namespace hpg

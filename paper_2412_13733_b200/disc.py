@@ -1,0 +1,488 @@
+"""Device-backed discretisations: the reference's solver-facing API on the B200 path.
+
+``ObstacleDisc2D`` / ``GradientDisc2D`` mirror ``hpgalerkin/assembly.py:452-603``
+and ``:699-860`` for the hot-path members: the same constructor arguments,
+the same method names, the same argument meaning and the same returned arrays
+(global x-major psi order, interior U order, cell order (cx, cy) cx-major).
+Every computation runs in ``libhpg_b200.so`` (sm_100a CUDA kernels behind the
+C ABI of ``include/hpg_b200.h``); there is no CPU fallback.
+
+Two API levels:
+
+* reference-facing (NumPy in / NumPy out, host buffers): ``exp_moments``,
+  ``nl_moments``, ``apply_D``, ``assemble_D``, ``data_moments``,
+  ``moments_from_values``, ``load_vector`` and ``proximal.residual`` -- the
+  drop-in seam;
+* device-resident (torch CUDA tensors, asynchronous on the current stream):
+  the ``*_t`` methods, used by the benchmark and by callers that keep the
+  Newton state on the GPU.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .tables import Tables
+
+F64 = torch.float64
+
+
+def _vp(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise _lib.HpgError("paper_2412_13733_b200 needs a CUDA device (no CPU fallback)")
+
+
+class Plan:
+    """Owns one ``hpgPlan`` (device tables + geometry + workspaces)."""
+
+    def __init__(self, kind, ncx, ncy, p, tables, hx, hy):
+        _require_cuda()
+        lib = _lib.load()
+        self._lib = lib
+        arrs = [np.ascontiguousarray(a, dtype=np.float64)
+                for a in (tables.S, tables.T, tables.Su, tables.Tu, hx, hy)]
+        h = ctypes.c_void_p()
+        _lib.call("hpgPlanCreate", ctypes.byref(h), kind, ncx, ncy, p, tables.nq,
+                  *[a.ctypes.data_as(ctypes.c_void_p) for a in arrs])
+        self.handle = h
+        info = (ctypes.c_longlong * 10)()
+        _lib.call("hpgPlanInfo", h, info)
+        (self.n, self.m, self.nq, self.ncells, self.ndof_psi, self.ndof_u,
+         self.wcache_len, self.block_len, self.path, self.splits) = [int(v) for v in info]
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.hpgPlanDestroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class _DeviceDisc:
+    dim = 2
+
+    def __init__(self, mesh2d, f, phi, f_mode="pointwise", phi_mode="pointwise",
+                 rule="reference", nq=None):
+        _require_cuda()
+        mx, my = mesh2d.mesh_x, mesh2d.mesh_y
+        degs = np.unique(np.concatenate([np.asarray(mx.degrees), np.asarray(my.degrees)]))
+        if self.kind == "obstacle" and np.any(degs < 2):
+            raise ValueError("obstacle discretization requires p >= 2")
+        if degs.size != 1:
+            raise ValueError("the B200 path needs one polynomial degree on every cell "
+                             f"(got degrees {degs.tolist()})")
+        self.mesh = mesh2d
+        self.p = int(degs[0])
+        self.n = self.p - 1 if self.kind == "obstacle" else self.p
+        self.m = self.p + 1
+        self.rule = rule
+        self.tables = Tables(rule, self.p, self.n, nq)
+        self.xpts = np.asarray(mx.points, dtype=float)
+        self.ypts = np.asarray(my.points, dtype=float)
+        self.ncx = self.xpts.size - 1
+        self.ncy = self.ypts.size - 1
+        self.hx = np.diff(self.xpts)
+        self.hy = np.diff(self.ypts)
+        kind = _lib.HPG_OBSTACLE if self.kind == "obstacle" else _lib.HPG_GRADIENT
+        self.plan = Plan(kind, self.ncx, self.ncy, self.p, self.tables, self.hx, self.hy)
+        self.nquad = self.tables.nq
+        self.ncomp_dofs = self.ncx * self.n * self.ncy * self.n
+        self.ndof_psi = self.plan.ndof_psi
+        self.ndof_u = self.plan.ndof_u
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._wcache = torch.empty(self.plan.wcache_len, dtype=F64, device=self.device)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._pinned = {}
+        self._devbuf = {}
+        self._cell_psi_indices = None
+        wx = np.concatenate([h / (2.0 * np.arange(self.n) + 1.0) for h in self.hx])
+        wy = np.concatenate([h / (2.0 * np.arange(self.n) + 1.0) for h in self.hy])
+        mass = np.kron(wx, wy)
+        self.mass_psi = mass if self.kind == "obstacle" else np.concatenate([mass, mass])
+        self.f_load_t = self.load_vector_t(self.sample_t(f, f_mode))
+        self.f_load = self.f_load_t.cpu().numpy()
+
+    # ------------------------------------------------------------------ layout
+    @property
+    def cell_ids(self):
+        return [(cx, cy) for cx in range(self.ncx) for cy in range(self.ncy)]
+
+    def _scalar_cell_indices(self):
+        n, ndof_y = self.n, self.ncy * self.n
+        ax = np.arange(n)
+        out = []
+        for cx in range(self.ncx):
+            ix = (cx * n + ax) * ndof_y
+            for cy in range(self.ncy):
+                out.append(np.add.outer(ix, cy * n + ax).ravel())
+        return out
+
+    @property
+    def cell_psi_indices(self):
+        """Global psi indices per cell, in cell order (``assembly.py:489,744``)."""
+        if self._cell_psi_indices is None:
+            sc = self._scalar_cell_indices()
+            if self.kind == "obstacle":
+                self._cell_psi_indices = sc
+            else:
+                self._cell_psi_indices = [np.concatenate([i, i + self.ncomp_dofs]) for i in sc]
+        return self._cell_psi_indices
+
+    def quad_grids(self):
+        """Per-cell (x axis, y axis) quadrature points, in cell order (``assembly.py:524``)."""
+        gx, gy = self._grids()
+        return [(gx[cx], gy[cy]) for cx, cy in self.cell_ids]
+
+    def _grids(self):
+        t = self.tables
+        gx = np.stack([t.points(self.xpts[i], self.xpts[i + 1]) for i in range(self.ncx)])
+        gy = np.stack([t.points(self.ypts[i], self.ypts[i + 1]) for i in range(self.ncy)])
+        return gx, gy
+
+    # --------------------------------------------------------------- transfers
+    def _pin(self, tag, n):
+        b = self._pinned.get(tag)
+        if b is None or b.numel() < n:
+            b = torch.empty(max(n, 1), dtype=F64, pin_memory=True)
+            self._pinned[tag] = b
+        return b[:n]
+
+    def _dev(self, tag, n):
+        b = self._devbuf.get(tag)
+        if b is None or b.numel() < n:
+            b = torch.empty(max(n, 1), dtype=F64, device=self.device)
+            self._devbuf[tag] = b
+        return b[:n]
+
+    def h2d(self, arr, tag):
+        """Host array -> device tensor through a reusable pinned staging buffer."""
+        a = np.ascontiguousarray(arr, dtype=np.float64).reshape(-1)
+        pin = self._pin("in_" + tag, a.size)
+        pin.numpy()[:] = a
+        dev = self._dev("in_" + tag, a.size)
+        dev.copy_(pin, non_blocking=True)
+        return dev
+
+    def d2h(self, t, tag):
+        pin = self._pin("out_" + tag, t.numel())
+        pin.copy_(t.reshape(-1), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return pin.numpy().copy()
+
+    def _check_len(self, v, n, what):
+        if v.numel() != n:
+            raise ValueError(f"{what} has {v.numel()} entries, expected {n}")
+
+    # ------------------------------------------------------------- data terms
+    def sample(self, g, mode="pointwise"):
+        """Point samples (ncells, nq, nq) of scalar data (``assembly.py:301-317``)."""
+        nq = self.nquad
+        shape = (self.ncx, self.ncy, nq, nq)
+        if np.isscalar(g):
+            return np.full(shape, float(g))
+        gx, gy = self._grids()
+        if mode == "cellwise":
+            mx = 0.5 * (self.xpts[:-1] + self.xpts[1:])
+            my = 0.5 * (self.ypts[:-1] + self.ypts[1:])
+            vals = np.asarray(g(mx[:, None], my[None, :]), dtype=float)
+            return np.broadcast_to(vals[:, :, None, None], shape).copy()
+        X = np.broadcast_to(gx[:, None, :, None], shape)
+        Y = np.broadcast_to(gy[None, :, None, :], shape)
+        return np.array(np.broadcast_to(np.asarray(g(X, Y), dtype=float), shape), copy=True)
+
+    def sample_t(self, g, mode="pointwise"):
+        vals = self.sample(g, mode)
+        return torch.from_numpy(vals.reshape(-1)).to(self.device)
+
+    def moments_from_values_t(self, vals_t, out=None):
+        out = torch.empty(self.ncomp_dofs, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgMomentsFromValues", self.plan.handle, _vp(vals_t), _vp(out), _stream())
+        return out
+
+    def load_vector_t(self, vals_t, out=None):
+        out = torch.empty(self.ndof_u, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgLoadVector", self.plan.handle, _vp(vals_t), _vp(out), _stream())
+        return out
+
+    def data_moments(self, g, mode="pointwise"):
+        """(g, zeta_i) over psi dofs (``assembly.py:514-519``)."""
+        return self.moments_from_values_t(self.sample_t(g, mode)).cpu().numpy()
+
+    def moments_from_values(self, values):
+        """From per-cell grid samples in cell order (``assembly.py:528-533``)."""
+        vals = np.ascontiguousarray(np.stack([np.asarray(v, dtype=float) for v in values]))
+        return self.moments_from_values_t(torch.from_numpy(vals.reshape(-1)).to(self.device)).cpu().numpy()
+
+    def load_vector(self, f, mode="pointwise"):
+        """(f, v_i) over interior U dofs (``assembly.py:502-512``)."""
+        return self.load_vector_t(self.sample_t(f, mode)).cpu().numpy()
+
+    # ---------------------------------------------------------- u-side pieces
+    def BT_u_t(self, u_t, out=None):
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgBTu", self.plan.handle, _vp(u_t), _vp(out), _stream())
+        return out
+
+    def B_psi_t(self, psi_t, out=None):
+        out = torch.empty(self.ndof_u, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgBPsi", self.plan.handle, _vp(psi_t), _vp(out), _stream())
+        return out
+
+    def A_u_t(self, u_t, out=None):
+        out = torch.empty(self.ndof_u, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgAu", self.plan.handle, _vp(u_t), _vp(out), _stream())
+        return out
+
+    # --------------------------------------------------------------- Jacobian
+    def apply_cached_t(self, x_t, out=None, wcache=None):
+        """D x from the weights cached by the last moments/residual call."""
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        w = self._wcache if wcache is None else wcache
+        _lib.call("hpgApplyCached", self.plan.handle, _vp(w), _vp(x_t), _vp(out), _stream())
+        return out
+
+    def blocks_t(self, wcache=None, out=None, c0=0, count=None):
+        count = self.plan.ncells - c0 if count is None else count
+        nb2 = self.plan.block_len
+        out = torch.empty((count, nb2), dtype=F64, device=self.device) if out is None else out
+        w = self._wcache if wcache is None else wcache
+        _lib.call("hpgBlocks", self.plan.handle, _vp(w), _vp(out), c0, count, _stream())
+        return out
+
+    def blocks_matvec_t(self, blocks_t, x_t, out=None):
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgBlocksMatvec", self.plan.handle, _vp(blocks_t), _vp(x_t), _vp(out), _stream())
+        return out
+
+    def assemble_D(self, psi):
+        """Element blocks of D as a device-backed CellBlockMatrix (``assembly.py:550-557``)."""
+        psi_t = self.h2d(psi, "psi")
+        clamped = self._weights_t(psi_t)
+        w = self._wcache.clone()
+        return DeviceCellBlockMatrix(self, w, bool(clamped.item()) if clamped is not None else False)
+
+    def assemble_D_t(self, psi_t):
+        clamped = self._weights_t(psi_t)
+        return DeviceCellBlockMatrix(self, self._wcache.clone(), clamped)
+
+    def _residual_t(self, alpha, psi_prev_t, u_t, psi_t, phi_t, b_u=None, b_psi=None, wcache=None,
+                    flag=None):
+        for v, n, what in ((psi_prev_t, self.ndof_psi, "psi_prev"), (u_t, self.ndof_u, "u"),
+                           (psi_t, self.ndof_psi, "psi")):
+            self._check_len(v, n, what)
+        b_u = torch.empty(self.ndof_u, dtype=F64, device=self.device) if b_u is None else b_u
+        b_psi = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if b_psi is None else b_psi
+        flag = self._flag if flag is None else flag
+        flag.zero_()
+        w = self._wcache if wcache is None else wcache
+        _lib.call("hpgResidual", self.plan.handle, float(alpha), _vp(psi_prev_t), _vp(u_t),
+                  _vp(psi_t), _vp(phi_t), _vp(self.f_load_t), _vp(b_u), _vp(b_psi), _vp(flag),
+                  _vp(w), _stream())
+        return b_u, b_psi, flag
+
+
+class ObstacleDisc2D(_DeviceDisc):
+    """Device-backed ``hpgalerkin.assembly.ObstacleDisc2D`` (``assembly.py:452-603``).
+
+    Extra keyword arguments: ``rule`` ("reference" = 2(p+1) Chebyshev-Lobatto
+    projection quadrature as the reference; "gauss" = ``nq``-point Gauss).
+    """
+
+    kind = "obstacle"
+    ncomp = 1
+
+    def __init__(self, mesh2d, f, phi, f_mode="pointwise", phi_mode="pointwise",
+                 rule="reference", nq=None):
+        super().__init__(mesh2d, f, phi, f_mode, phi_mode, rule, nq)
+        self.phi_moments_t = self.moments_from_values_t(self.sample_t(phi, phi_mode))
+
+    @property
+    def phi_moments(self):
+        return self.phi_moments_t.cpu().numpy()
+
+    @phi_moments.setter
+    def phi_moments(self, value):
+        # QVI overwrites the obstacle moments between solves (qvi.py:205)
+        v = np.ascontiguousarray(value, dtype=np.float64).reshape(-1)
+        if v.size != self.ndof_psi:
+            raise ValueError("phi_moments has the wrong length")
+        self.phi_moments_t = torch.from_numpy(v).to(self.device)
+
+    # device-resident API
+    def exp_moments_t(self, psi_t, out=None, wcache=None, flag=None):
+        """Returns (moments, device clamp flag); also refreshes the weight cache."""
+        self._check_len(psi_t, self.ndof_psi, "psi")
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        flag = self._flag if flag is None else flag
+        flag.zero_()
+        w = self._wcache if wcache is None else wcache
+        _lib.call("hpgObstacleMoments", self.plan.handle, _vp(psi_t), _vp(out), _vp(flag),
+                  _vp(w), _stream())
+        return out, flag
+
+    def apply_D_t(self, psi_t, x_t, out=None):
+        self._check_len(psi_t, self.ndof_psi, "psi")
+        self._check_len(x_t, self.ndof_psi, "x")
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgObstacleApplyD", self.plan.handle, _vp(psi_t), _vp(x_t), _vp(out), _stream())
+        return out
+
+    def residual_t(self, alpha, psi_prev_t, u_t, psi_t, **kw):
+        return self._residual_t(alpha, psi_prev_t, u_t, psi_t, self.phi_moments_t, **kw)
+
+    def _weights_t(self, psi_t):
+        tmp = self._dev("moments_scratch", self.ndof_psi)
+        _, flag = self.exp_moments_t(psi_t, out=tmp)
+        return flag
+
+    # reference-facing API
+    def exp_moments(self, psi):
+        """((e^{-psi}, zeta_i), clamped) -- ``assembly.py:541-548``."""
+        out, flag = self.exp_moments_t(self.h2d(psi, "psi"), out=self._dev("out_moments", self.ndof_psi))
+        res = self.d2h(out, "moments")
+        return res, bool(flag.item())
+
+    def apply_D(self, psi, x):
+        """``assembly.py:559-567``."""
+        y = self.apply_D_t(self.h2d(psi, "psi"), self.h2d(x, "x"), out=self._dev("out_y", self.ndof_psi))
+        return self.d2h(y, "y")
+
+
+class GradientDisc2D(_DeviceDisc):
+    """Device-backed ``hpgalerkin.assembly.GradientDisc2D`` (``assembly.py:699-860``)."""
+
+    kind = "gradient"
+    ncomp = 2
+
+    def __init__(self, mesh2d, f, phi, f_mode="pointwise", phi_mode="pointwise",
+                 rule="reference", nq=None):
+        super().__init__(mesh2d, f, phi, f_mode, phi_mode, rule, nq)
+        self.phi_values_t = self.sample_t(phi, phi_mode)
+
+    @property
+    def cell_scalar_indices(self):
+        return self._scalar_cell_indices()
+
+    @property
+    def phi_values(self):
+        """dict cell -> (nq, nq) samples, as ``assembly.py:747-748``."""
+        v = self.phi_values_t.cpu().numpy().reshape(self.plan.ncells, self.nquad, self.nquad)
+        return {c: v[i] for i, c in enumerate(self.cell_ids)}
+
+    def nl_moments_t(self, psi_t, out=None, wcache=None):
+        self._check_len(psi_t, self.ndof_psi, "psi")
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        w = self._wcache if wcache is None else wcache
+        _lib.call("hpgGradientMoments", self.plan.handle, _vp(psi_t), _vp(self.phi_values_t),
+                  _vp(out), _vp(w), _stream())
+        return out
+
+    def apply_D_t(self, psi_t, x_t, out=None):
+        self._check_len(psi_t, self.ndof_psi, "psi")
+        self._check_len(x_t, self.ndof_psi, "x")
+        out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
+        _lib.call("hpgGradientApplyD", self.plan.handle, _vp(psi_t), _vp(self.phi_values_t),
+                  _vp(x_t), _vp(out), _stream())
+        return out
+
+    def residual_t(self, alpha, psi_prev_t, u_t, psi_t, **kw):
+        return self._residual_t(alpha, psi_prev_t, u_t, psi_t, self.phi_values_t, **kw)
+
+    def _weights_t(self, psi_t):
+        tmp = self._dev("moments_scratch", self.ndof_psi)
+        self.nl_moments_t(psi_t, out=tmp)
+        return None
+
+    def nl_moments(self, psi):
+        """(phi psi_c / sqrt(1+|psi|^2), zeta_i) stacked -- ``assembly.py:781-791``."""
+        out = self.nl_moments_t(self.h2d(psi, "psi"), out=self._dev("out_moments", self.ndof_psi))
+        return self.d2h(out, "moments")
+
+    def apply_D(self, psi, x):
+        """``assembly.py:817-832``."""
+        y = self.apply_D_t(self.h2d(psi, "psi"), self.h2d(x, "x"), out=self._dev("out_y", self.ndof_psi))
+        return self.d2h(y, "y")
+
+
+class DeviceCellBlockMatrix:
+    """``CellBlockMatrix`` (``assembly.py:272-298``) whose state lives on the GPU.
+
+    It holds the point weights of D(psi).  ``@``/``matvec`` run the fused
+    matrix-free kernel on those weights -- the same linear operator as the
+    dense blocks (``apply_weighted == weighted_block @ c``,
+    ``tests/test_assembly.py:126-132``).  The dense per-cell blocks are built
+    on the device only when ``blocks`` / ``blocks_t`` / ``tocsc`` are asked for.
+    """
+
+    def __init__(self, disc, wcache, clamped):
+        self.disc = disc
+        self._w = wcache
+        self._clamped = clamped
+        self._blocks_t = None
+        self._blocks_host = None
+        self.n = disc.ndof_psi
+
+    @property
+    def clamped(self):
+        c = self._clamped
+        if isinstance(c, torch.Tensor):
+            c = bool(c.item())
+            self._clamped = c
+        return bool(c)
+
+    @property
+    def indices(self):
+        return self.disc.cell_psi_indices
+
+    @property
+    def nb(self):
+        return self.disc.n * self.disc.n * self.disc.ncomp
+
+    def blocks_t(self):
+        if self._blocks_t is None:
+            self._blocks_t = self.disc.blocks_t(wcache=self._w).view(-1, self.nb, self.nb)
+        return self._blocks_t
+
+    @property
+    def blocks(self):
+        if self._blocks_host is None:
+            arr = self.blocks_t().cpu().numpy()
+            self._blocks_host = [arr[i] for i in range(arr.shape[0])]
+        return self._blocks_host
+
+    def matvec_t(self, x_t, out=None):
+        return self.disc.apply_cached_t(x_t, out=out, wcache=self._w)
+
+    def matvec_blocks_t(self, x_t, out=None):
+        return self.disc.blocks_matvec_t(self.blocks_t(), x_t, out=out)
+
+    def matvec(self, x):
+        d = self.disc
+        y = self.matvec_t(d.h2d(x, "x"), out=d._dev("out_y", self.n))
+        return d.d2h(y, "y")
+
+    def tocsc(self):
+        import scipy.sparse as sp
+        rows, cols, vals = [], [], []
+        for blk, idx in zip(self.blocks, self.indices):
+            jj, kk = np.meshgrid(idx, idx, indexing="ij")
+            rows.append(jj.ravel())
+            cols.append(kk.ravel())
+            vals.append(blk.ravel())
+        return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                             shape=(self.n, self.n)).tocsc()
+
+    def __matmul__(self, x):
+        return self.matvec(x)
