@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 element-quadrature-points/s for residual + Jacobian apply.
+
+Metric (BASELINE.json): EQP/s = N * Q^2 * (1 + k_mv) / t for
+one "step" = 1 LVPP residual (proximal.residual: b_u, b_psi, clamp flag) +
+k_mv Jacobian matvecs D(psi) x, on synthetic seeded inputs with the config's
+shapes (no public dataset exists for this path).  Default workload: config 1
+(64x64 mesh, p=16, Q=24 Gauss, 1 residual + 50 matvecs, alpha cycling over
+{1, 4, 16}) -- the largest single-GPU configuration BASELINE.json quotes.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
+
+Prints ONE JSON line on rank 0.  ``value`` is device-timed (CUDA events on the
+launching stream, inputs resident in HBM, L2 flushed between timed steps);
+``e2e`` is the same metric through the reference-facing NumPy API with host
+buffers (H2D/D2H inside the timed region).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2412_13733_b200.workloads import CONFIGS, config_inputs  # noqa: E402
+
+METRIC = "fp64 element-quadrature-points/sec for residual+Jacobian apply"
+UNIT = "EQP/s"
+P_FP64_TFLOPS = 37.17       # measured DMMA peak, profiles/fp64_peaks_r01.json
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def peaks():
+    hbm = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        hbm = 6650.0
+    return hbm
+
+
+def syn_flops(n, Q):
+    return 2.0 * Q * n * (n + Q)
+
+
+def algorithmic(cfg, disc_n, nq, ndof_psi, ndof_u):
+    """SURVEY.md §8d canonical flops/bytes per residual and per matvec."""
+    N = cfg.N
+    nc = cfg.ncomp
+    F_res = N * 2 * nc * syn_flops(disc_n, nq)
+    F_mv = N * nc * 2 * syn_flops(disc_n, nq)
+    phi_in = N * disc_n * disc_n if cfg.kind == "obstacle" else N * nq * nq
+    B_res = 8.0 * (ndof_u + 2 * ndof_psi + phi_in + ndof_psi + ndof_u + ndof_u)
+    B_mv = 8.0 * 2 * ndof_psi
+    return F_res, F_mv, B_res, B_mv
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_step(cfg, rule, cells_frac=None):
+    """One bounded sample of the workload on the CPU oracle (numpy port of the
+    reference's per-cell algorithm, oracle/hpg_oracle.py).  Returns
+    (seconds, eqp_in_sample, sample description)."""
+    from types import SimpleNamespace
+
+    from oracle import hpg_oracle as orc
+    from paper_2412_13733_b200.tables import Tables
+    nc_full = cfg.ncells
+    # bound the sample: at most ~4096 cells x 8 matvecs of c1 size
+    ncells = nc_full
+    kmv = cfg.k_mv
+    if cfg.name == "c1":
+        kmv = 5
+    if cfg.name.startswith("c4"):
+        ncells = 64
+    t = Tables(rule, cfg.p, cfg.n, cfg.nq(rule))
+    tt = SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq)
+    x = np.linspace(0.0, 1.0, ncells + 1)
+    P = orc.Problem(cfg.kind, x, x, cfg.p, tt)
+    inp = config_inputs(cfg, ncells=ncells)
+    phi_vals = P.sample(inp["phi"])
+    f_load = P.load_vector(P.sample(1.0))
+    if cfg.kind == "obstacle":
+        phi_mom = P.data_moments(phi_vals)
+    t0 = time.perf_counter()
+    if cfg.kind == "obstacle":
+        P.residual(cfg.alphas[0], inp["psi_prev"], inp["u"], inp["psi"], f_load, phi_moments=phi_mom)
+        for _ in range(kmv):
+            P.obstacle_apply_D(inp["psi"], inp["x"])
+    else:
+        P.residual(cfg.alphas[0], inp["psi_prev"], inp["u"], inp["psi"], f_load, phi_vals=phi_vals)
+        for _ in range(kmv):
+            P.gradient_apply_D(inp["psi"], inp["x"], phi_vals)
+    dt = time.perf_counter() - t0
+    eqp = ncells * ncells * t.nq ** 2 * (1 + kmv)
+    desc = (f"oracle (numpy port of hpgalerkin per-cell quadrature, batched over cells) on "
+            f"{ncells}x{ncells} cells of {cfg.name} (p={cfg.p}, {rule} rule nq={t.nq}): "
+            f"1 residual + {kmv} apply_D")
+    return dt, eqp, desc
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    rule = args.rule
+    for _ in range(args.warmup):
+        cpu_reference_step(cfg, rule)
+    times, eqps = [], []
+    desc = ""
+    for _ in range(args.steps):
+        dt, eqp, desc = cpu_reference_step(cfg, rule)
+        times.append(dt)
+        eqps.append(eqp)
+    value = sum(eqps) / sum(times)
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8d)",
+        "config": {"workload": f"{cfg.name} {cfg.kind} {cfg.ncells}x{cfg.ncells} p={cfg.p} "
+                               f"{rule} nq={cfg.nq(rule)}: 1 residual + {cfg.k_mv} matvecs",
+                   "rule": rule},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--rule", default="gauss", choices=["gauss", "reference"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    from paper_2412_13733_b200.proximal import residual
+
+    rule = args.rule
+    nq = cfg.nq(rule)
+    inp = config_inputs(cfg, seed=rank)       # each rank: its own slab of elements (weak scaling)
+    mesh = uniform_mesh_2d(0.0, 1.0, cfg.ncells, cfg.p)
+    cls = D.ObstacleDisc2D if cfg.kind == "obstacle" else D.GradientDisc2D
+    disc = cls(mesh, inp["f"], inp["phi"], rule=rule, nq=nq if rule == "gauss" else None)
+    dev = disc.device
+    psi = torch.from_numpy(inp["psi"]).to(dev)
+    psi_prev = torch.from_numpy(inp["psi_prev"]).to(dev)
+    u = torch.from_numpy(inp["u"]).to(dev)
+    x = torch.from_numpy(inp["x"]).to(dev)
+    b_u = torch.empty(disc.ndof_u, dtype=torch.float64, device=dev)
+    b_psi = torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev)
+    y = torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    cached = not cfg.name.startswith("c4")      # c4: HBM-bound, recompute weights from psi
+    kmv = cfg.k_mv
+    reps = cfg.reps
+
+    def step_residual(alpha):
+        if cached:
+            disc.residual_t(alpha, psi_prev, u, psi, b_u=b_u, b_psi=b_psi, flag=flag)
+        else:
+            _res_nocache(alpha)
+
+    def _res_nocache(alpha):
+        from paper_2412_13733_b200 import _lib
+        from paper_2412_13733_b200.disc import _stream, _vp
+        flag.zero_()
+        phi_t = disc.phi_moments_t if cfg.kind == "obstacle" else disc.phi_values_t
+        _lib.call("hpgResidual", disc.plan.handle, float(alpha), _vp(psi_prev), _vp(u), _vp(psi),
+                  _vp(phi_t), _vp(disc.f_load_t), _vp(b_u), _vp(b_psi), _vp(flag), None, _stream())
+
+    def step_matvecs():
+        for _ in range(kmv):
+            if cached:
+                disc.apply_cached_t(x, out=y)
+            else:
+                disc.apply_D_t(psi, x, out=y)
+
+    # per-alpha graphs: residual, then matvecs (captured once each)
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        for a in cfg.alphas:
+            step_residual(a)
+        step_matvecs()
+    torch.cuda.synchronize()
+    g_res = {}
+    for a in cfg.alphas:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(reps if not cached else 1):
+                step_residual(a)
+                if not cached:
+                    disc.apply_D_t(psi, x, out=y)
+        g_res[a] = g
+    g_mv = None
+    if cached:
+        g_mv = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_mv, stream=stream):
+            step_matvecs()
+    torch.cuda.synchronize()
+
+    launches_per_residual = 3 + (1 if disc.plan.splits > 1 and disc.plan.path == 1 else 0)
+    launches_per_step = (launches_per_residual + kmv) * (1 if cached else reps)
+
+    def run_steps(nsteps, timed):
+        evs = []
+        for s in range(nsteps):
+            a = cfg.alphas[s % len(cfg.alphas)]
+            flush.fill_(float(s))                  # evict L2 between steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g_res[a].replay()
+            e1.record(stream)
+            if g_mv is not None:
+                g_mv.replay()
+            e2.record(stream)
+            evs.append((e0, e1, e2))
+        return evs
+
+    with torch.cuda.stream(stream):
+        run_steps(args.warmup, False)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            evs = run_steps(args.steps, True)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    step_ms = [e0.elapsed_time(e2) for e0, e1, e2 in evs]
+    res_ms = [e0.elapsed_time(e1) for e0, e1, e2 in evs]
+    mv_ms = [e1.elapsed_time(e2) for e0, e1, e2 in evs] if cached else None
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    eqp_step = cfg.N * nq * nq * (1 + kmv) * reps
+    value = eqp_step * args.steps * world / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel
+    F_res, F_mv, B_res, B_mv = algorithmic(cfg, disc.n, nq, disc.ndof_psi, disc.ndof_u)
+    hbm = peaks()
+    if cached:
+        t_k = statistics.mean(mv_ms) / kmv * 1e-3
+        achieved = F_mv / t_k / 1e12
+        roof = {"kernel": "k_warp<NT,QT,M_OBST_CACHED> (Jacobian apply from cached weights)"
+                if cfg.kind == "obstacle" else "Jacobian apply from cached weights (gradient)",
+                "bound": "tensor", "achieved": achieved, "peak": P_FP64_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / P_FP64_TFLOPS, "traffic": None,
+                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peaks_r01.json)",
+                "algorithmic_per_launch": {"flops": F_mv, "bytes": B_mv},
+                "avg_launch_us": t_k * 1e6}
+    else:
+        t_k = statistics.mean(res_ms) / reps * 1e-3       # fused residual + apply per rep
+        bytes_ = B_res + B_mv
+        achieved = bytes_ / t_k / 1e9
+        roof = {"kernel": "residual (k_warp M_OBST_RES + u-side) + apply (k_warp M_OBST_APPLY) per rep",
+                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic_per_launch": {"flops": F_res + F_mv, "bytes": bytes_},
+                "avg_launch_us": t_k * 1e6}
+    # roofline-combined lower bound for the whole step
+    t_lb = max((F_res + kmv * F_mv) / (P_FP64_TFLOPS * 1e12), (B_res + kmv * B_mv) / (hbm * 1e9)) * reps
+    step_frac = t_lb / (statistics.mean(step_ms) * 1e-3)
+
+    # e2e through the reference-facing NumPy API (host buffers)
+    e2e = None
+    if args.e2e_steps > 0:
+        hp = {k: np.ascontiguousarray(inp[k]) for k in ("psi", "psi_prev", "u", "x")}
+        torch.cuda.synchronize()
+        t_e2e = []
+        for s in range(args.e2e_steps + 1):
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                bu_h, bpsi_h, cl = residual(disc, cfg.alphas[s % len(cfg.alphas)], hp["psi_prev"],
+                                            hp["u"], hp["psi"])
+                Dm = disc.assemble_D(hp["psi"]) if cached else None
+                for _ in range(kmv):
+                    y_h = (Dm @ hp["x"]) if cached else disc.apply_D(hp["psi"], hp["x"])
+            torch.cuda.synchronize()
+            if s > 0:
+                t_e2e.append(time.perf_counter() - t0)
+        h2d = 8 * reps * (2 * disc.ndof_psi + disc.ndof_u + (disc.ndof_psi if cached else 0)
+                          + kmv * disc.ndof_psi * (1 if cached else 2))
+        d2h = 8 * reps * (disc.ndof_u + disc.ndof_psi + kmv * disc.ndof_psi) + 4 * reps
+        e2e = {"value": eqp_step / statistics.mean(t_e2e) * world, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": 1e3 * statistics.mean(t_e2e),
+               "path": "paper_2412_13733_b200.proximal.residual + disc.assemble_D + (D @ x) x k_mv, NumPy in/out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            dt, eqp, desc = cpu_reference_step(cfg, rule)
+            cpu = {"value": eqp / dt, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                   "sample": desc, "seconds": dt}
+        except Exception as exc:      # the baseline must never sink the GPU line
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded inputs with the config's shapes and value laws, SURVEY.md §8d)",
+            "config": {"workload": f"{cfg.name}: {cfg.kind} {cfg.ncells}x{cfg.ncells} cells, p={cfg.p}, "
+                                   f"{rule} rule nq={nq}, (1 residual + {kmv} Jacobian matvecs)"
+                                   + (f" x {reps}" if reps > 1 else "")
+                                   + (f", alpha cycling {list(cfg.alphas)}" if len(cfg.alphas) > 1 else ""),
+                       "rule": rule, "ncells": cfg.N, "p": cfg.p, "nq": nq, "k_mv": kmv, "reps": reps,
+                       "matvec": "cached point weights" if cached else "weights recomputed from psi",
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "eqp_per_step": eqp_step},
+            "roofline": roof,
+            "step_roofline_frac": step_frac,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "res_ms_mean": statistics.mean(res_ms),
+            "mv_ms_mean": statistics.mean(mv_ms) if mv_ms else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,8 @@ struct hpgPlan_st {
   double* partial = nullptr;    // CTA split partials
   size_t partial_len = 0;
   double* Z = nullptr;          // blocks stage-1 scratch
+  double* edge = nullptr;       // [N][4m-4] residual hat contributions
+  double* ubuf = nullptr;       // CTA path U-side scratch (large m)
   int zcells = 0;
   int* dflag = nullptr;
   int nsm = 148;
@@ -207,6 +209,7 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   cudaError_t e = cudaMalloc(&P->scratch_u, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
   if (e == cudaSuccess) e = cudaMalloc(&P->mu, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
   if (e == cudaSuccess) e = cudaMalloc(&P->dflag, sizeof(int) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&P->edge, sizeof(double) * (size_t)P->N * (4 * P->m - 4) + 16);
   if (e != cudaSuccess) { delete P; return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
 
   // path selection
@@ -238,7 +241,7 @@ int hpgPlanDestroy(hpgPlan P) {
   if (P == nullptr) return HPG_OK;
   cudaFree(P->Sf); cudaFree(P->Tf); cudaFree(P->hx); cudaFree(P->hy); cudaFree(P->G);
   cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
-  cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag);
+  cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag); cudaFree(P->edge); cudaFree(P->ubuf);
   delete P;
   return HPG_OK;
 }
@@ -313,6 +316,18 @@ int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u
   cudaStream_t s = (cudaStream_t)stream;
   ElemArgs A = base_args(P);
   A.in0 = psi; A.out = b_psi; A.wc_out = wcache; A.residual = 1; A.u = u;
+  A.alpha = alpha; A.psi_prev = psi_prev; A.f_load = f_load; A.b_u = b_u; A.edge = P->edge;
+  A.usmem = 4 * P->m * (P->m | 1) + 2 * P->n * P->n;
+  {
+    // CTA path with large tiles: U-side buffers in global scratch (L2 resident)
+    int mode = P->kind == HPG_OBSTACLE ? M_OBST_RES : M_GRAD_RES;
+    int nin = P->kind == HPG_OBSTACLE ? 1 : 2, nout = nin;
+    size_t base = (size_t)nin * P->NP * (P->NP + 2) + (size_t)(nin * P->NT + nout * P->QT + nout * P->NT) * 64;
+    if (!P->use_warp[mode] && (base + A.usmem) * sizeof(double) > 200 * 1024) {
+      if (P->ubuf == nullptr) CUDA_TRY(cudaMalloc(&P->ubuf, sizeof(double) * (size_t)P->N * A.usmem + 16));
+      A.ubuf = P->ubuf;
+    }
+  }
   int rc;
   if (P->kind == HPG_OBSTACLE) {
     if (!clamped) return fail(HPG_ERR_ARG, "null clamp flag");
@@ -323,10 +338,12 @@ int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u
     rc = run_elem<M_GRAD_RES>(P, A, s);
   }
   if (rc) return rc;
-  UArgs U = base_uargs(P);
-  U.u = u; U.ca = -alpha; U.psi_a = psi_prev; U.psi_b = psi;
-  U.base = f_load; U.cbase = alpha; U.out = b_u;
-  return run_ulocal(P, U, s);
+  long long nh = (long long)(P->ncx - 1) * P->niy + (long long)(P->nix - (P->ncx - 1)) * (P->ncy - 1);
+  if (nh > 0) {
+    k_hat_gather<<<(unsigned)((nh + 255) / 256), 256, 0, s>>>(A);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return HPG_OK;
 }
 
 int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {

@@ -62,7 +62,7 @@ __device__ __forceinline__ void gemm_store(const GemmArgs& g, int batch, int i, 
     int cx = e / g.ncy, cy = e - cx * g.ncy;
     int a = i / g.n, jj = i - a * g.n;     // row (a, j) of Z
     int bb = j / g.n, kk = j - bb * g.n;   // col (b, k) of G
-    double wa = g.hx[cx] / (2.0 * a + 1.0), wb = g.hy[cy] / (2.0 * bb + 1.0);
+    double wa = g.hx[cx] * kInvOdd[a], wb = g.hy[cy] * kInvOdd[bb];
     double val = v * (wa * wb);
     long long row = (long long)a * g.n + bb, col = (long long)jj * g.n + kk;
     double* blk = g.out + (long long)cl * g.nb * g.nb;

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "hpg_invodd.cuh"
+
 namespace hpg {
 
 constexpr double EXP_CLAMP = 700.0;   // hpgalerkin/assembly.py:25
@@ -61,7 +63,32 @@ struct ElemArgs {
   int NT, QT, splits;
   double* partial;   // [N][splits][NOUT][NP*NP] when splits > 1
   int out_cellmajor; // M_VALUES for the u side: out is (N, n, n) cell-major
+  // fused residual U side (hpg_ucell.cuh)
+  double alpha;
+  const double* psi_prev;
+  const double* f_load;
+  double* b_u;
+  double* edge;      // [N][4m-4] hat-involved local contributions
+  int usmem;         // doubles of U-side shared memory per thread group
+  double* ubuf;      // CTA path, large m: U-side buffers in global scratch [N][usmem]
 };
+
+struct WarpSync { __device__ __forceinline__ void operator()() const { __syncwarp(); } };
+struct BlockSync { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
+
+// 1D interior dof -> contributing (cell, local index) pairs, fixed order.
+__device__ __forceinline__ int u_owners_1d_dev(int i, int nc, int p, int* cell, int* loc) {
+  if (i < nc - 1) {
+    int v = i + 1;
+    cell[0] = v - 1; loc[0] = 1;
+    cell[1] = v; loc[1] = 0;
+    return 2;
+  }
+  int b = i - (nc - 1);
+  cell[0] = b / (p - 1);
+  loc[0] = 2 + b % (p - 1);
+  return 1;
+}
 
 enum Mode : int {
   M_OBST_RES = 0,     // psi -> exp moments (+ weight cache, flag)
@@ -108,8 +135,8 @@ __device__ __forceinline__ int legendre_row(int a, int p, int* col, double* coef
   int k = 0;
   if (a == 0) { col[k] = 0; coef[k++] = 0.5; col[k] = 1; coef[k++] = 0.5; }
   if (a == 1) { col[k] = 0; coef[k++] = -0.5; col[k] = 1; coef[k++] = 0.5; }
-  if (a <= p - 2) { col[k] = 2 + a; coef[k++] = 1.0 / (2 * a + 3); }
-  if (a >= 2 && a - 2 <= p - 2) { col[k] = a; coef[k++] = -1.0 / (2 * a - 1); }
+  if (a <= p - 2) { col[k] = 2 + a; coef[k++] = kInvOdd[a + 1]; }
+  if (a >= 2 && a - 2 <= p - 2) { col[k] = a; coef[k++] = -kInvOdd[a - 1]; }
   return k;
 }
 
@@ -140,8 +167,8 @@ __device__ __forceinline__ double btu_value(const ElemArgs& A, bool gradient, in
     s += ai[x] * t;
   }
   double fa = wa, fb = wb;
-  if (gradient && comp == 0) fa = 2.0 / (2 * a + 1);
-  if (gradient && comp == 1) fb = 2.0 / (2 * b + 1);
+  if (gradient && comp == 0) fa = 2.0 * kInvOdd[a];
+  if (gradient && comp == 1) fb = 2.0 * kInvOdd[b];
   return (fa * s) * fb;
 }
 

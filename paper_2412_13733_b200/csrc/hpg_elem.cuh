@@ -13,6 +13,7 @@
 #pragma once
 #include "hpg_common.cuh"
 #include "hpg_pointmap.cuh"
+#include "hpg_ucell.cuh"
 
 namespace hpg {
 
@@ -37,10 +38,10 @@ __device__ __forceinline__ long long wc_index(int e, int QT, int rt, int ht, int
 // Final value of moment (a, b), output component o, of cell e.
 template <int MODE>
 __device__ __forceinline__ void write_moment(const ElemArgs& A, int e, int cx, int cy, int o,
-                                             int a, int b, double y) {
+                                             int a, int b, double y, const double* sBTu = nullptr) {
   constexpr bool gradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
-  double wa = A.hx[cx] / (2.0 * a + 1.0);
-  double wb = A.hy[cy] / (2.0 * b + 1.0);
+  double wa = A.hx[cx] * kInvOdd[a];
+  double wb = A.hy[cy] * kInvOdd[b];
   double val = (wa * y) * wb;
   if (A.out_cellmajor) {
     A.out[((long long)e * A.n + a) * A.n + b] = val;
@@ -49,7 +50,8 @@ __device__ __forceinline__ void write_moment(const ElemArgs& A, int e, int cx, i
   long long idx = (long long)o * A.ncomp + psi_index(A, cx, cy, a, b);
   if (A.residual) {
     // proximal.py:123 / :125
-    double btu = btu_value(A, gradient, o, cx, cy, a, b, wa, wb);
+    double btu = sBTu != nullptr ? sBTu[(o * A.n + a) * A.n + b]
+                                 : btu_value(A, gradient, o, cx, cy, a, b, wa, wb);
     if constexpr (gradient) val = val - btu;
     else val = (__ldg(A.phi_mom + idx) - btu) - val;
   }
@@ -136,6 +138,9 @@ k_warp(ElemArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
   double* sTile = sT + NP * QP + warp * (NIN > 0 ? NIN * TILE : 0);
+  double* sU = sT + NP * QP + WARP_CTA_WARPS * NIN * TILE + warp * A.usmem;
+  constexpr bool kResidual = MODE == M_OBST_RES || MODE == M_GRAD_RES;
+  constexpr bool kGradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
   for (int i = threadIdx.x; i < QP * NP; i += blockDim.x) {
     sS[i] = A.Sf[i];
     sT[i] = A.Tf[i];
@@ -158,6 +163,14 @@ k_warp(ElemArgs A) {
       }
     }
     __syncwarp();
+    const double* sBTu = nullptr;
+    if constexpr (kResidual) {
+      if (A.residual) {
+        double* btu = sU + 4 * A.m * ucell_ld(A.m);
+        ucell_residual<kGradient>(A, e, cx, cy, sTile, sTile + TILE, LDT, sU, btu, lane, 32, WarpSync{});
+        sBTu = btu;
+      }
+    }
 
     double Y[NOUT][NT][NT][2];
 #pragma unroll
@@ -233,7 +246,7 @@ k_warp(ElemArgs A) {
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             int a = 8 * at + 2 * c + j, b = 8 * bt + r;
-            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j]);
+            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j], sBTu);
           }
     __syncwarp();
   }
@@ -257,11 +270,15 @@ k_cta(ElemArgs A) {
   double* sP = sTile + NIN * TILE;               // [NSYN][NT][64]
   double* sV = sP + NSYN * NT * 64;               // [NOUT][QT][64]
   double* sR = sV + NOUT * QT * 64;               // [NOUT][NT][64]
+  constexpr bool kResidual = MODE == M_OBST_RES || MODE == M_GRAD_RES;
+  constexpr bool kGradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
   const int e = blockIdx.x / A.splits, sp = blockIdx.x - e * A.splits;
   if (e >= A.N) return;
   const int rt0 = (sp * QT) / A.splits, rt1 = ((sp + 1) * QT) / A.splits;
+  double* sU = A.ubuf != nullptr ? A.ubuf + (long long)e * A.usmem   // U side (residual only)
+                                 : sR + NOUT * NT * 64;
   const int cx = e / A.ncy, cy = e - cx * A.ncy;
 
   for (int f = 0; f < NIN; ++f) {
@@ -277,6 +294,16 @@ k_cta(ElemArgs A) {
     }
   }
   __syncthreads();
+  const double* sBTu = nullptr;
+  if constexpr (kResidual) {
+    // U side once per element: by the CTA holding the first row-tile split
+    if (A.residual && sp == 0) {
+      double* btu = sU + 4 * A.m * ucell_ld(A.m);
+      ucell_residual<kGradient>(A, e, cx, cy, sTile, sTile + TILE, LDT, sU, btu, threadIdx.x,
+                                blockDim.x, BlockSync{});
+      sBTu = btu;
+    }
+  }
 
   const int ny = NOUT * NT * NT;
   double Y[MAXS][2];
@@ -352,7 +379,7 @@ k_cta(ElemArgs A) {
       for (int j = 0; j < 2; ++j) {
         int a = 8 * at + 2 * c + j, b = 8 * bt + r;
         if (A.splits == 1) {
-          if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[s][j]);
+          if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[s][j], sBTu);
         } else {
           A.partial[(((long long)e * A.splits + sp) * NOUT + o) * NP * NP + a * NP + b] = Y[s][j];
         }

@@ -11,14 +11,27 @@ template <int NT, int QT, int MODE>
 int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
   constexpr int NP = 8 * NT, QP = 8 * QT;
-  constexpr size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * TR::NIN * NP * (NP + 2));
-  static bool attr = false;
-  if (!attr) {
+  const size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * TR::NIN * NP * (NP + 2) +
+                                        (size_t)WARP_CTA_WARPS * A.usmem);
+  if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "warp path shared memory too large");
+  static size_t attr = 0;
+  if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(k_warp<NT, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_warp)", e);
-    attr = true;
+    attr = smem;
   }
-  int grid = (A.N + WARP_CTA_WARPS - 1) / WARP_CTA_WARPS;
+  // persistent-style grid: every resident warp slot gets an equal share of cells
+  static int occ = -1, nsm = 0, occ_smem = -1;
+  if (occ < 0 || occ_smem != (int)smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp<NT, QT, MODE>, 32 * WARP_CTA_WARPS, smem);
+    if (occ < 1) occ = 1;
+    occ_smem = (int)smem;
+  }
+  int need = (A.N + WARP_CTA_WARPS - 1) / WARP_CTA_WARPS;
+  int grid = need < nsm * occ ? need : nsm * occ;
   k_warp<NT, QT, MODE><<<grid, 32 * WARP_CTA_WARPS, smem, s>>>(A);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_warp launch", e);
@@ -29,7 +42,8 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
   const int NP = 8 * A.NT;
   size_t smem = sizeof(double) * ((size_t)TR::NIN * NP * (NP + 2) +
-                                  (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64);
+                                  (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64 +
+                                  (A.ubuf != nullptr ? 0 : (size_t)A.usmem));
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "element tile too large for shared memory");
   static int attr = 0;
   if ((int)smem > attr) {

@@ -182,19 +182,6 @@ __global__ void k_u_local(UArgs U) {
   U.scratch[tid] = val;
 }
 
-// 1D interior dof -> contributing (cell, local index) pairs, fixed order.
-__device__ __forceinline__ int u_owners_1d(int i, int nc, int p, int* cell, int* loc) {
-  if (i < nc - 1) {
-    int v = i + 1;
-    cell[0] = v - 1; loc[0] = 1;
-    cell[1] = v; loc[1] = 0;
-    return 2;
-  }
-  int b = i - (nc - 1);
-  cell[0] = b / (p - 1);
-  loc[0] = 2 + b % (p - 1);
-  return 1;
-}
 
 __global__ void k_u_gather(UArgs U) {
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -202,8 +189,8 @@ __global__ void k_u_gather(UArgs U) {
   if (tid >= total) return;
   int iy = tid % U.niy, ix = (int)(tid / U.niy);
   int cxs[2], jx[2], cys[2], ky[2];
-  int nx = u_owners_1d(ix, U.ncx, U.p, cxs, jx);
-  int ny = u_owners_1d(iy, U.ncy, U.p, cys, ky);
+  int nx = u_owners_1d_dev(ix, U.ncx, U.p, cxs, jx);
+  int ny = u_owners_1d_dev(iy, U.ncy, U.p, cys, ky);
   const int m = U.m;
   double s = 0.0;
   for (int a = 0; a < nx; ++a)

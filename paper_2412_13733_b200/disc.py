@@ -106,6 +106,7 @@ class _DeviceDisc:
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._pinned = {}
         self._devbuf = {}
+        self._events = {}
         self._cell_psi_indices = None
         wx = np.concatenate([h / (2.0 * np.arange(self.n) + 1.0) for h in self.hx])
         wy = np.concatenate([h / (2.0 * np.arange(self.n) + 1.0) for h in self.hy])
@@ -170,9 +171,15 @@ class _DeviceDisc:
         """Host array -> device tensor through a reusable pinned staging buffer."""
         a = np.ascontiguousarray(arr, dtype=np.float64).reshape(-1)
         pin = self._pin("in_" + tag, a.size)
+        ev = self._events.get(tag)
+        if ev is not None:
+            ev.synchronize()      # the previous async copy out of this buffer is done
         pin.numpy()[:] = a
         dev = self._dev("in_" + tag, a.size)
         dev.copy_(pin, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._events[tag] = ev
         return dev
 
     def d2h(self, t, tag):
