@@ -12,6 +12,7 @@
 #include "hpg_common.cuh"
 #include "hpg_launch.cuh"
 #include "hpg_useside.cuh"
+#include "hpg_ucell.cuh"
 
 using namespace hpg;
 
@@ -83,6 +84,7 @@ struct hpgPlan_st {
   double* Z = nullptr;          // blocks stage-1 scratch
   double* edge = nullptr;       // [N][4m-4] residual hat contributions
   double* ubuf = nullptr;       // CTA path U-side scratch (large m)
+
   int zcells = 0;
   int* dflag = nullptr;
   int nsm = 148;
@@ -317,26 +319,32 @@ int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u
   ElemArgs A = base_args(P);
   A.in0 = psi; A.out = b_psi; A.wc_out = wcache; A.residual = 1; A.u = u;
   A.alpha = alpha; A.psi_prev = psi_prev; A.f_load = f_load; A.b_u = b_u; A.edge = P->edge;
-  A.usmem = 4 * P->m * (P->m | 1) + 2 * P->n * P->n;
-  {
-    // CTA path with large tiles: U-side buffers in global scratch (L2 resident)
-    int mode = P->kind == HPG_OBSTACLE ? M_OBST_RES : M_GRAD_RES;
-    int nin = P->kind == HPG_OBSTACLE ? 1 : 2, nout = nin;
-    size_t base = (size_t)nin * P->NP * (P->NP + 2) + (size_t)(nin * P->NT + nout * P->QT + nout * P->NT) * 64;
-    if (!P->use_warp[mode] && (base + A.usmem) * sizeof(double) > 200 * 1024) {
-      if (P->ubuf == nullptr) CUDA_TRY(cudaMalloc(&P->ubuf, sizeof(double) * (size_t)P->N * A.usmem + 16));
-      A.ubuf = P->ubuf;
-    }
-  }
   int rc;
   if (P->kind == HPG_OBSTACLE) {
     if (!clamped) return fail(HPG_ERR_ARG, "null clamp flag");
     A.phi_mom = phi; A.flag = clamped;
-    rc = run_elem<M_OBST_RES>(P, A, s);
   } else {
     A.phi = phi; A.flag = P->dflag;
-    rc = run_elem<M_GRAD_RES>(P, A, s);
   }
+  {
+    // (1) U side (thread per cell-local entry): b_psi <- phi_mom - B^T u
+    //     (obstacle) | -B^T u (gradient); b_u on owned dofs + edge scratch
+    int threads = P->m * P->m;
+    threads = threads > 1024 ? 1024 : ((threads + 31) / 32) * 32;
+    size_t smem = sizeof(double) * ((size_t)P->m * (P->m | 1) + 2 * (size_t)P->n * P->n + 2 * P->m + 8);
+    if (smem > ((size_t)227 << 10)) return fail(HPG_ERR_UNSUPPORTED, "U tile too large for shared memory");
+    void* fn = P->kind == HPG_GRADIENT ? (void*)k_uside_pt<true> : (void*)k_uside_pt<false>;
+    if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ElemArgs U = A;
+    void* args[] = {&U};
+    CUDA_TRY(cudaLaunchKernel(fn, dim3(P->N), dim3(threads), args, smem, s));
+    CUDA_TRY(cudaGetLastError());
+  }
+  // (2) psi side finishes b_psi in place (proximal.py:123 order)
+  A.residual = 2;
+  A.usmem = 0;
+  A.ubuf = nullptr;
+  rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, A, s) : run_elem<M_GRAD_RES>(P, A, s);
   if (rc) return rc;
   long long nh = (long long)(P->ncx - 1) * P->niy + (long long)(P->nix - (P->ncx - 1)) * (P->ncy - 1);
   if (nh > 0) {

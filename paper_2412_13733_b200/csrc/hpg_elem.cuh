@@ -38,17 +38,23 @@ __device__ __forceinline__ long long wc_index(int e, int QT, int rt, int ht, int
 // Final value of moment (a, b), output component o, of cell e.
 template <int MODE>
 __device__ __forceinline__ void write_moment(const ElemArgs& A, int e, int cx, int cy, int o,
-                                             int a, int b, double y, const double* sBTu = nullptr) {
+                                             int a, int b, double y, const double* sBTu = nullptr,
+                                             const double* inv = kInvOdd) {
   constexpr bool gradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
-  double wa = A.hx[cx] * kInvOdd[a];
-  double wb = A.hy[cy] * kInvOdd[b];
+  double wa = A.hx[cx] * inv[a];
+  double wb = A.hy[cy] * inv[b];
   double val = (wa * y) * wb;
   if (A.out_cellmajor) {
     A.out[((long long)e * A.n + a) * A.n + b] = val;
     return;
   }
   long long idx = (long long)o * A.ncomp + psi_index(A, cx, cy, a, b);
-  if (A.residual) {
+  if (A.residual == 2) {
+    // b_psi already holds phi_moments - B^T u (obstacle) / -B^T u (gradient)
+    // from k_ucell: finish proximal.py:123 / :125 in the reference's order
+    if constexpr (gradient) val = A.out[idx] + val;
+    else val = A.out[idx] - val;
+  } else if (A.residual) {
     // proximal.py:123 / :125
     double btu = sBTu != nullptr ? sBTu[(o * A.n + a) * A.n + b]
                                  : btu_value(A, gradient, o, cx, cy, a, b, wa, wb);
@@ -138,13 +144,15 @@ k_warp(ElemArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
   double* sTile = sT + NP * QP + warp * (NIN > 0 ? NIN * TILE : 0);
-  double* sU = sT + NP * QP + WARP_CTA_WARPS * NIN * TILE + warp * A.usmem;
+  double* sInv = sT + NP * QP + WARP_CTA_WARPS * NIN * TILE;      // 1/(2k+1), k < NP
+  double* sU = sInv + NP + warp * A.usmem;
   constexpr bool kResidual = MODE == M_OBST_RES || MODE == M_GRAD_RES;
   constexpr bool kGradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
   for (int i = threadIdx.x; i < QP * NP; i += blockDim.x) {
     sS[i] = A.Sf[i];
     sT[i] = A.Tf[i];
   }
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
   __syncthreads();
 
   for (int e = blockIdx.x * WARP_CTA_WARPS + warp; e < A.N; e += gridDim.x * WARP_CTA_WARPS) {
@@ -165,7 +173,7 @@ k_warp(ElemArgs A) {
     __syncwarp();
     const double* sBTu = nullptr;
     if constexpr (kResidual) {
-      if (A.residual) {
+      if (A.residual == 1) {
         double* btu = sU + 4 * A.m * ucell_ld(A.m);
         ucell_residual<kGradient>(A, e, cx, cy, sTile, sTile + TILE, LDT, sU, btu, lane, 32, WarpSync{});
         sBTu = btu;
@@ -246,7 +254,7 @@ k_warp(ElemArgs A) {
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             int a = 8 * at + 2 * c + j, b = 8 * bt + r;
-            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j], sBTu);
+            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j], sBTu, sInv);
           }
     __syncwarp();
   }
@@ -297,7 +305,7 @@ k_cta(ElemArgs A) {
   const double* sBTu = nullptr;
   if constexpr (kResidual) {
     // U side once per element: by the CTA holding the first row-tile split
-    if (A.residual && sp == 0) {
+    if (A.residual == 1 && sp == 0) {
       double* btu = sU + 4 * A.m * ucell_ld(A.m);
       ucell_residual<kGradient>(A, e, cx, cy, sTile, sTile + TILE, LDT, sU, btu, threadIdx.x,
                                 blockDim.x, BlockSync{});

@@ -11,7 +11,7 @@ template <int NT, int QT, int MODE>
 int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
   constexpr int NP = 8 * NT, QP = 8 * QT;
-  const size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * TR::NIN * NP * (NP + 2) +
+  const size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * TR::NIN * NP * (NP + 2) + NP +
                                         (size_t)WARP_CTA_WARPS * A.usmem);
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "warp path shared memory too large");
   static size_t attr = 0;
