@@ -85,6 +85,14 @@ int hpgResidual(hpgPlan plan, double alpha, const double* psi_prev,
                 const double* f_load, double* b_u, double* b_psi,
                 int* clamped, double* wcache, void* stream);
 
+/* Residual plus the Jacobian apply y = D(psi) x at the same psi (the Newton
+ * step's residual and first Krylov matvec), sharing one pass over psi on the
+ * low-degree path.  Same arguments as hpgResidual plus x and y. */
+int hpgResidualApply(hpgPlan plan, double alpha, const double* psi_prev,
+                     const double* u, const double* psi, const double* phi,
+                     const double* f_load, const double* x, double* b_u,
+                     double* b_psi, double* y, int* clamped, void* stream);
+
 /* Element blocks (assembly.py:550-557 / 804-815) from cached weights:
  * blocks[ncells][nb][nb], nb = n^2 (obstacle) or 2 n^2 (gradient),
  * row = a*n+b (test), col = j*n+k (trial).  Cells [c0, c0+count). */

@@ -29,6 +29,7 @@ SIGNATURES = {
     "hpgGradientApplyD": [_P, _P, _P, _P, _P, _P],
     "hpgApplyCached": [_P, _P, _P, _P, _P],
     "hpgResidual": [_P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "hpgResidualApply": [_P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "hpgBlocks": [_P, _P, _P, _I, _I, _P],
     "hpgBlocksMatvec": [_P, _P, _P, _P, _P],
     "hpgBTu": [_P, _P, _P, _P],

@@ -12,6 +12,7 @@
 #include "hpg_common.cuh"
 #include "hpg_launch.cuh"
 #include "hpg_useside.cuh"
+#include "hpg_small.cuh"
 #include "hpg_ucell.cuh"
 
 using namespace hpg;
@@ -84,6 +85,8 @@ struct hpgPlan_st {
   double* Z = nullptr;          // blocks stage-1 scratch
   double* edge = nullptr;       // [N][4m-4] residual hat contributions
   double* ubuf = nullptr;       // CTA path U-side scratch (large m)
+  bool small = false;           // thread-per-element low-degree path available
+  SmallTables stab;             // its tables (kernel-parameter / constant bank)
 
   int zcells = 0;
   int* dflag = nullptr;
@@ -200,6 +203,15 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   std::vector<double> suf = pk_table(Su, nq, P->m, P->QT, 8 * P->NTu);
   if ((rc = upload(&P->Tuf, tuf.data(), tuf.size()))) { delete P; return rc; }
   if ((rc = upload(&P->Suf, suf.data(), suf.size()))) { delete P; return rc; }
+  // low-degree obstacle path (config 4): tables passed by value to k_small
+  memset(&P->stab, 0, sizeof(P->stab));
+  if (kind == HPG_OBSTACLE && P->n <= SMALL_MAXN && nq <= SMALL_MAXQ && small_available(P->n, nq)) {
+    P->small = true;
+    for (int g = 0; g < nq; ++g)
+      for (int a = 0; a < P->n; ++a) P->stab.S[g * P->n + a] = S[(size_t)g * P->n + a];
+    for (int a = 0; a < P->n; ++a)
+      for (int g = 0; g < nq; ++g) P->stab.T[a * nq + g] = T[(size_t)a * nq + g];
+  }
   // block table G[(a,j)][g] = T[a][g] S[g][j]
   int n2 = P->n * P->n;
   std::vector<double> G((size_t)n2 * P->QP, 0.0);
@@ -271,6 +283,7 @@ int hpgObstacleMoments(hpgPlan P, const double* psi, double* out, int* clamped, 
   if (!psi || !out || !clamped) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
   A.in0 = psi; A.out = out; A.flag = clamped; A.wc_out = wcache;
+  if (P->small && wcache == nullptr) return run_small(P->n, P->nq, true, false, A, P->stab, (cudaStream_t)stream);
   return run_elem<M_OBST_RES>(P, A, (cudaStream_t)stream);
 }
 
@@ -280,6 +293,10 @@ int hpgObstacleApplyD(hpgPlan P, const double* psi, const double* x, double* y, 
   if (!psi || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
   A.in0 = psi; A.in1 = x; A.out = y;
+  if (P->small) {
+    A.wc_out = y;
+    return run_small(P->n, P->nq, false, true, A, P->stab, (cudaStream_t)stream);
+  }
   return run_elem<M_OBST_APPLY>(P, A, (cudaStream_t)stream);
 }
 
@@ -310,9 +327,10 @@ int hpgApplyCached(hpgPlan P, const double* wcache, const double* x, double* y, 
   return run_elem<M_GRAD_CACHED>(P, A, (cudaStream_t)stream);
 }
 
-int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u, const double* psi,
-                const double* phi, const double* f_load, double* b_u, double* b_psi, int* clamped,
-                double* wcache, void* stream) {
+static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const double* u,
+                         const double* psi, const double* phi, const double* f_load, double* b_u,
+                         double* b_psi, int* clamped, double* wcache, const double* x, double* y,
+                         void* stream) {
   if (int rc = check(P)) return rc;
   if (!psi_prev || !u || !psi || !phi || !f_load || !b_u || !b_psi) return fail(HPG_ERR_ARG, "null pointer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -329,29 +347,60 @@ int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u
   {
     // (1) U side (thread per cell-local entry): b_psi <- phi_mom - B^T u
     //     (obstacle) | -B^T u (gradient); b_u on owned dofs + edge scratch
-    int threads = P->m * P->m;
-    threads = threads > 1024 ? 1024 : ((threads + 31) / 32) * 32;
-    size_t smem = sizeof(double) * ((size_t)P->m * (P->m | 1) + 2 * (size_t)P->n * P->n + 2 * P->m + 8);
+    int TG = P->m * P->m;
+    TG = TG > 1024 ? 1024 : ((TG + 31) / 32) * 32;
+    int cpb = 256 / TG;
+    if (cpb < 1) cpb = 1;
+    size_t smem = sizeof(double) * ((size_t)cpb * ((size_t)P->m * (P->m | 1) + 2 * (size_t)P->n * P->n) +
+                                    2 * P->m + 8);
     if (smem > ((size_t)227 << 10)) return fail(HPG_ERR_UNSUPPORTED, "U tile too large for shared memory");
     void* fn = P->kind == HPG_GRADIENT ? (void*)k_uside_pt<true> : (void*)k_uside_pt<false>;
     if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ElemArgs U = A;
-    void* args[] = {&U};
-    CUDA_TRY(cudaLaunchKernel(fn, dim3(P->N), dim3(threads), args, smem, s));
+    void* args[] = {&U, &cpb, &TG};
+    CUDA_TRY(cudaLaunchKernel(fn, dim3((P->N + cpb - 1) / cpb), dim3(cpb * TG), args, smem, s));
     CUDA_TRY(cudaGetLastError());
   }
   // (2) psi side finishes b_psi in place (proximal.py:123 order)
   A.residual = 2;
   A.usmem = 0;
   A.ubuf = nullptr;
-  rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, A, s) : run_elem<M_GRAD_RES>(P, A, s);
+  if (P->small && wcache == nullptr) {
+    // low-degree path: one thread per cell, residual moments (+ Jacobian apply
+    // at the same psi when x is given) in a single pass over psi
+    if (x != nullptr) { A.in1 = x; A.wc_out = y; }
+    rc = run_small(P->n, P->nq, true, x != nullptr, A, P->stab, s);
+    x = nullptr;
+  } else {
+    rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, A, s) : run_elem<M_GRAD_RES>(P, A, s);
+  }
   if (rc) return rc;
   long long nh = (long long)(P->ncx - 1) * P->niy + (long long)(P->nix - (P->ncx - 1)) * (P->ncy - 1);
   if (nh > 0) {
     k_hat_gather<<<(unsigned)((nh + 255) / 256), 256, 0, s>>>(A);
     CUDA_TRY(cudaGetLastError());
   }
+  if (x != nullptr) {
+    // Jacobian apply at the same psi (not fused on this path)
+    if (P->kind == HPG_OBSTACLE) return hpgObstacleApplyD(P, psi, x, y, stream);
+    return hpgGradientApplyD(P, psi, phi, x, y, stream);
+  }
   return HPG_OK;
+}
+
+int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u, const double* psi,
+                const double* phi, const double* f_load, double* b_u, double* b_psi, int* clamped,
+                double* wcache, void* stream) {
+  return residual_impl(P, alpha, psi_prev, u, psi, phi, f_load, b_u, b_psi, clamped, wcache, nullptr,
+                       nullptr, stream);
+}
+
+int hpgResidualApply(hpgPlan P, double alpha, const double* psi_prev, const double* u, const double* psi,
+                     const double* phi, const double* f_load, const double* x, double* b_u,
+                     double* b_psi, double* y, int* clamped, void* stream) {
+  if (!x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  return residual_impl(P, alpha, psi_prev, u, psi, phi, f_load, b_u, b_psi, clamped, nullptr, x, y,
+                       stream);
 }
 
 int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {

@@ -16,4 +16,9 @@ template <int MODE> bool warp_available(int NT, int QT);
 // with A.splits row-tile splits + deterministic reduction).
 template <int MODE> int run_mode(bool use_warp, ElemArgs A, cudaStream_t s);
 
+// Thread-per-element low-degree obstacle kernel (hpg_small.cuh).
+struct SmallTables;
+bool small_available(int n, int q);
+int run_small(int n, int q, bool res, bool apply, const ElemArgs& A, const SmallTables& tb, cudaStream_t s);
+
 }  // namespace hpg

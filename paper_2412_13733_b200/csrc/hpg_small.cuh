@@ -1,0 +1,128 @@
+// Thread-per-element kernel for the low-degree, HBM-bound regime (config 4:
+// p = 2/4/6, 65,536 cells).  Tensor-core tiles would be mostly padding here
+// (n = 1..5, Q = 5..14), so each thread owns one cell and runs the
+// sum-factorised chain on the FP64 FMA pipe with the 1D tables in the kernel
+// parameter (constant) bank: every table operand is a uniform constant-bank
+// operand of a DFMA, no loads at all.
+//
+//   per point row g:  P[b]  = sum_a S[g][a] C[a][b]           (C: psi tile)
+//                     V[h]  = sum_b P[b] S[h][b]    -> E = exp(min(-V, 700)) (+flag)
+//                     Vx[h] = same on the direction tile X  (apply)
+//                     e[b]  = sum_h E[h] T[b][h],  ex[b] = sum_h E[h] Vx[h] T[b][h]
+//                     M[a][b]  += T[a][g] e[b],  MY[a][b] += T[a][g] ex[b]
+// then b_psi (in place, after the U-side kernel) -= w_a w_b M and
+// y = w_a w_b MY -- one pass over psi and x serves residual and Jacobian apply.
+#pragma once
+#include "hpg_common.cuh"
+
+namespace hpg {
+
+constexpr int SMALL_MAXN = 8, SMALL_MAXQ = 16, SMALL_THREADS = 128;
+
+struct SmallTables {
+  double S[SMALL_MAXQ * SMALL_MAXN];   // S[g][a], row-major (Q x N)
+  double T[SMALL_MAXN * SMALL_MAXQ];   // T[a][g], row-major (N x Q)
+};
+
+// RES: residual moments (b_psi RMW, A.residual == 2) or plain moments (out);
+// APPLY: y = D(psi) x into A.wc_out (reused as the y pointer).
+template <int N, bool APPLY>
+__host__ __device__ constexpr int small_threads() {
+  return (APPLY ? 2 : 1) * N * N * SMALL_THREADS * 8 <= 48 * 1024 ? SMALL_THREADS : SMALL_THREADS / 2;
+}
+
+template <int N, int Q, bool RES, bool APPLY>
+__global__ void __launch_bounds__(small_threads<N, APPLY>()) k_small(ElemArgs A, const SmallTables tb) {
+  constexpr int NIN = APPLY ? 2 : 1;
+  constexpr int TH = small_threads<N, APPLY>();
+  __shared__ double sC[NIN][N * N][TH];     // thread-private tile slices
+  const int tid = threadIdx.x;
+  const int e = blockIdx.x * TH + tid;
+  if (e >= A.N) return;
+  const int cx = e / A.ncy, cy = e - cx * A.ncy;
+  const long long base = psi_index(A, cx, cy, 0, 0);
+#pragma unroll
+  for (int a = 0; a < N; ++a)
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      sC[0][a * N + b][tid] = __ldg(A.in0 + base + (long long)a * A.ld + b);
+      if (APPLY) sC[NIN - 1][a * N + b][tid] = __ldg(A.in1 + base + (long long)a * A.ld + b);
+    }
+  double M[RES ? N : 1][RES ? N : 1];
+  double MY[APPLY ? N : 1][APPLY ? N : 1];
+#pragma unroll
+  for (int a = 0; a < N; ++a)
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      if (RES) M[a][b] = 0.0;
+      if (APPLY) MY[a][b] = 0.0;
+    }
+  bool flag = false;
+#pragma unroll 1
+  for (int g = 0; g < Q; ++g) {
+    double P[N], PX[APPLY ? N : 1];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double s = 0.0, sx = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        s = fma(tb.S[g * N + a], sC[0][a * N + b][tid], s);
+        if (APPLY) sx = fma(tb.S[g * N + a], sC[NIN - 1][a * N + b][tid], sx);
+      }
+      P[b] = s;
+      if (APPLY) PX[b] = sx;
+    }
+    double ev[N], exv[APPLY ? N : 1];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      ev[b] = 0.0;
+      if (APPLY) exv[b] = 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < Q; ++h) {
+      double v = 0.0, vx = 0.0;
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        v = fma(P[b], tb.S[h * N + b], v);
+        if (APPLY) vx = fma(PX[b], tb.S[h * N + b], vx);
+      }
+      bool fl = false;
+      const double E = clamped_exp_neg(v, fl);
+      flag |= fl;
+      const double Ex = E * vx;
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        if (RES) ev[b] = fma(E, tb.T[b * Q + h], ev[b]);
+        if (APPLY) exv[b] = fma(Ex, tb.T[b * Q + h], exv[b]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const double t = tb.T[a * Q + g];
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        if (RES) M[a][b] = fma(t, ev[b], M[a][b]);
+        if (APPLY) MY[a][b] = fma(t, exv[b], MY[a][b]);
+      }
+    }
+  }
+  if (RES && flag) atomicOr(A.flag, 1);
+  const double hx = A.hx[cx], hy = A.hy[cy];
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    const double wa = hx * kInvOdd[a];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      const double wb = hy * kInvOdd[b];
+      const long long g = base + (long long)a * A.ld + b;
+      if (RES) {
+        const double val = (wa * M[a][b]) * wb;
+        if (A.residual == 2) A.out[g] = A.out[g] - val;     // (phi - B^T u) - moments
+        else A.out[g] = val;
+      }
+      if (APPLY) A.wc_out[g] = (wa * MY[a][b]) * wb;
+    }
+  }
+}
+
+}  // namespace hpg

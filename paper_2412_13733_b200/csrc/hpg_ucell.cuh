@@ -474,22 +474,26 @@ __device__ __forceinline__ Sp3 k_row(int j, Inv inv_odd) {
 }
 
 template <bool GRADIENT>
-__global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A) {
+__global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG) {
+  // cpb cell groups of TG threads per CTA (small tiles share a CTA)
   extern __shared__ double smem[];
   const int m = A.m, n = A.n, p = A.p, ld = m | 1;
-  const int e = blockIdx.x;
-  const int cx = e / A.ncy, cy = e - cx * A.ncy;
+  const int grp = threadIdx.x / TG, t0 = threadIdx.x - grp * TG;
+  double* sI = smem;                                   // 1/(2k+1)
+  for (int t = threadIdx.x; t < 2 * m + 8; t += blockDim.x) sI[t] = kInvOdd[t];
+  const int e = blockIdx.x * cpb + grp;
+  const bool valid = grp < cpb && e < A.N;
+  const int ee = valid ? e : 0;
+  const int cx = ee / A.ncy, cy = ee - cx * A.ncy;
   const double hx = A.hx[cx], hy = A.hy[cy];
   const long long base0 = psi_index(A, cx, cy, 0, 0);
-  double* sC = smem;                      // m x ld local U tile
+  double* sC = smem + 2 * m + 8 + (size_t)(grp < cpb ? grp : 0) * (m * ld + 2 * n * n);  // m x ld U tile
   double* sG = sC + m * ld;               // [comp][n][n] weighted psi_prev - psi
-  double* sI = sG + 2 * n * n;            // 1/(2k+1)
-  for (int t = threadIdx.x; t < 2 * m + 8; t += blockDim.x) sI[t] = kInvOdd[t];
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+  for (int t = valid ? t0 : m * m; t < m * m; t += TG) {
     const int i = t / m, l = t - i * m;
     sC[i * ld + l] = u_at(A, cx, cy, i, l);
   }
-  for (int t = threadIdx.x; t < n * n * (GRADIENT ? 2 : 1); t += blockDim.x) {
+  for (int t = valid ? t0 : n * n * 2; t < n * n * (GRADIENT ? 2 : 1); t += TG) {
     const int comp = t / (n * n), r = t - comp * n * n, i = r / n, l = r - i * n;
     const long long gi = comp * A.ncomp + base0 + (long long)i * A.ld + l;
     const double d = __ldg(A.psi_prev + gi) - __ldg(A.in0 + gi);
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A) {
   __syncthreads();
   auto C = [&](int i, int l) { return sC[i * ld + l]; };
   auto inv = [&](int k) { return sI[k]; };
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+  for (int t = valid ? t0 : m * m; t < m * m; t += TG) {
     const int j = t / m, k = t - j * m;
     // A u (local) = (hy/hx) Kref C Mref + (hx/hy) Mref C Kref,
     // Mref = R^T diag(1/(2l+1)) R expanded as nested sparse sums

@@ -293,11 +293,27 @@ class _DeviceDisc:
         b_psi = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if b_psi is None else b_psi
         flag = self._flag if flag is None else flag
         flag.zero_()
-        w = self._wcache if wcache is None else wcache
+        if wcache is True:
+            wcache = self._wcache
         _lib.call("hpgResidual", self.plan.handle, float(alpha), _vp(psi_prev_t), _vp(u_t),
                   _vp(psi_t), _vp(phi_t), _vp(self.f_load_t), _vp(b_u), _vp(b_psi), _vp(flag),
-                  _vp(w), _stream())
+                  _vp(wcache), _stream())
         return b_u, b_psi, flag
+
+    def _residual_apply_t(self, alpha, psi_prev_t, u_t, psi_t, x_t, phi_t, b_u=None, b_psi=None,
+                          y=None, flag=None):
+        for v, n, what in ((psi_prev_t, self.ndof_psi, "psi_prev"), (u_t, self.ndof_u, "u"),
+                           (psi_t, self.ndof_psi, "psi"), (x_t, self.ndof_psi, "x")):
+            self._check_len(v, n, what)
+        b_u = torch.empty(self.ndof_u, dtype=F64, device=self.device) if b_u is None else b_u
+        b_psi = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if b_psi is None else b_psi
+        y = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if y is None else y
+        flag = self._flag if flag is None else flag
+        flag.zero_()
+        _lib.call("hpgResidualApply", self.plan.handle, float(alpha), _vp(psi_prev_t), _vp(u_t),
+                  _vp(psi_t), _vp(phi_t), _vp(self.f_load_t), _vp(x_t), _vp(b_u), _vp(b_psi), _vp(y),
+                  _vp(flag), _stream())
+        return b_u, b_psi, y, flag
 
 
 class ObstacleDisc2D(_DeviceDisc):
@@ -334,9 +350,10 @@ class ObstacleDisc2D(_DeviceDisc):
         out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
         flag = self._flag if flag is None else flag
         flag.zero_()
-        w = self._wcache if wcache is None else wcache
+        if wcache is True:
+            wcache = self._wcache
         _lib.call("hpgObstacleMoments", self.plan.handle, _vp(psi_t), _vp(out), _vp(flag),
-                  _vp(w), _stream())
+                  _vp(wcache), _stream())
         return out, flag
 
     def apply_D_t(self, psi_t, x_t, out=None):
@@ -347,11 +364,16 @@ class ObstacleDisc2D(_DeviceDisc):
         return out
 
     def residual_t(self, alpha, psi_prev_t, u_t, psi_t, **kw):
+        """``proximal.residual`` on device; ``wcache=True`` also caches D(psi)'s weights."""
         return self._residual_t(alpha, psi_prev_t, u_t, psi_t, self.phi_moments_t, **kw)
+
+    def residual_apply_t(self, alpha, psi_prev_t, u_t, psi_t, x_t, **kw):
+        """Residual and y = D(psi) x in one launch sequence (hpgResidualApply)."""
+        return self._residual_apply_t(alpha, psi_prev_t, u_t, psi_t, x_t, self.phi_moments_t, **kw)
 
     def _weights_t(self, psi_t):
         tmp = self._dev("moments_scratch", self.ndof_psi)
-        _, flag = self.exp_moments_t(psi_t, out=tmp)
+        _, flag = self.exp_moments_t(psi_t, out=tmp, wcache=True)
         return flag
 
     # reference-facing API
@@ -391,9 +413,10 @@ class GradientDisc2D(_DeviceDisc):
     def nl_moments_t(self, psi_t, out=None, wcache=None):
         self._check_len(psi_t, self.ndof_psi, "psi")
         out = torch.empty(self.ndof_psi, dtype=F64, device=self.device) if out is None else out
-        w = self._wcache if wcache is None else wcache
+        if wcache is True:
+            wcache = self._wcache
         _lib.call("hpgGradientMoments", self.plan.handle, _vp(psi_t), _vp(self.phi_values_t),
-                  _vp(out), _vp(w), _stream())
+                  _vp(out), _vp(wcache), _stream())
         return out
 
     def apply_D_t(self, psi_t, x_t, out=None):
@@ -407,9 +430,12 @@ class GradientDisc2D(_DeviceDisc):
     def residual_t(self, alpha, psi_prev_t, u_t, psi_t, **kw):
         return self._residual_t(alpha, psi_prev_t, u_t, psi_t, self.phi_values_t, **kw)
 
+    def residual_apply_t(self, alpha, psi_prev_t, u_t, psi_t, x_t, **kw):
+        return self._residual_apply_t(alpha, psi_prev_t, u_t, psi_t, x_t, self.phi_values_t, **kw)
+
     def _weights_t(self, psi_t):
         tmp = self._dev("moments_scratch", self.ndof_psi)
-        self.nl_moments_t(psi_t, out=tmp)
+        self.nl_moments_t(psi_t, out=tmp, wcache=True)
         return None
 
     def nl_moments(self, psi):

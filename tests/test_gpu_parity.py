@@ -106,3 +106,34 @@ def test_errors_are_loud():
     d = D.ObstacleDisc2D(uniform_mesh_2d(0.0, 1.0, 2, 3), 1.0, 1.0)
     with pytest.raises(ValueError):
         d.exp_moments(np.zeros(d.ndof_psi + 1))
+
+
+@pytest.mark.parametrize("name", [n for n in names() if n.startswith(("c4", "c0", "c1", "nonuni", "clamp", "grad"))])
+def test_residual_paths_and_fused_apply(name):
+    """All device routes agree with the reference: residual with the weight cache
+    (warp/CTA DMMA path), without it (thread-per-cell path where the degree is
+    low), the fused residual+apply entry point, and the cached Jacobian apply."""
+    import torch
+    g = load(name)
+    if np.isnan(g["psi"]).any():
+        pytest.skip("NaN case covered elsewhere")
+    d = make_disc(g)
+    t = {k: torch.from_numpy(np.ascontiguousarray(g[k])).cuda() for k in ("psi", "psi_prev", "u", "x")}
+    for kw in ({}, {"wcache": True}):
+        b_u, b_psi, flag = d.residual_t(g["alpha"], t["psi_prev"], t["u"], t["psi"], **kw)
+        assert rel_err(b_u.cpu().numpy(), g["b_u"]) < TOL
+        assert rel_err(b_psi.cpu().numpy(), g["b_psi"]) < TOL
+        if g["kind"] == "obstacle":
+            assert bool(flag.item()) == g["res_clamped"]
+    # the cache written by the last call serves the Jacobian apply
+    y = d.apply_cached_t(t["x"]).cpu().numpy()
+    assert rel_err(y, g["Dx"]) < TOL
+    b_u, b_psi, y, flag = d.residual_apply_t(g["alpha"], t["psi_prev"], t["u"], t["psi"], t["x"])
+    assert rel_err(b_u.cpu().numpy(), g["b_u"]) < TOL
+    assert rel_err(b_psi.cpu().numpy(), g["b_psi"]) < TOL
+    assert rel_err(y.cpu().numpy(), g["apply_D"]) < TOL
+    if g["kind"] == "obstacle":
+        m, _ = d.exp_moments_t(t["psi"])
+        assert rel_err(m.cpu().numpy(), g["moments"]) < TOL
+        m, _ = d.exp_moments_t(t["psi"], wcache=True)
+        assert rel_err(m.cpu().numpy(), g["moments"]) < TOL

@@ -27,7 +27,7 @@ def main():
     t = {k: torch.from_numpy(inp[k]).to(dev) for k in ("psi", "psi_prev", "u", "x")}
     torch.cuda.synchronize()
     for _ in range(3):
-        d.residual_t(cfg.alphas[0], t["psi_prev"], t["u"], t["psi"])
+        d.residual_t(cfg.alphas[0], t["psi_prev"], t["u"], t["psi"], wcache=True)
         d.apply_cached_t(t["x"])
         d.apply_D_t(t["psi"], t["x"])
         if blocks:
