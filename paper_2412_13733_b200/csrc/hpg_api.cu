@@ -344,7 +344,10 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
   } else {
     A.phi = phi; A.flag = P->dflag;
   }
-  {
+  if (usmall_available(P->p, P->kind == HPG_GRADIENT)) {
+    // (1) U side, low degree: thread per cell, generated straight-line code
+    if ((rc = run_usmall(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
+  } else {
     // (1) U side (thread per cell-local entry): b_psi <- phi_mom - B^T u
     //     (obstacle) | -B^T u (gradient); b_u on owned dofs + edge scratch
     int TG = P->m * P->m;

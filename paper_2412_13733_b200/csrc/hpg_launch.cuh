@@ -21,4 +21,8 @@ struct SmallTables;
 bool small_available(int n, int q);
 int run_small(int n, int q, bool res, bool apply, const ElemArgs& A, const SmallTables& tb, cudaStream_t s);
 
+// Thread-per-cell generated U side for low degrees (hpg_usmall.cu).
+bool usmall_available(int p, bool gradient);
+int run_usmall(int p, bool gradient, const ElemArgs& A, cudaStream_t s);
+
 }  // namespace hpg
