@@ -64,54 +64,56 @@ def algorithmic(cfg, disc_n, nq, ndof_psi, ndof_u):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled DURING the timed region
+    through NVML (nvidia-ml-py) every ~2 ms in a background thread; falls back
+    to `nvidia-smi -lms 100` when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
+        self.samples = []
+        self.reason_mask = 0
+        self.max_mhz = None
+        self._stop = None
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self._stop = threading.Event()
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        self.reason_mask |= int(get_reasons(h))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+
+            self._thread = threading.Thread(target=run, daemon=True)
+            self._thread.start()
         except Exception:
-            self.proc = None
+            self._stop = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                self.proc.kill()
-                out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._stop is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.reason_mask & bit)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML during the timed region"}
 
 
 def cpu_reference_step(cfg, rule, cells_frac=None):
@@ -165,6 +167,25 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def config_dict(cfg, rule):
+    """The workload description shared by both arms (same config => comparable)."""
+    nq = cfg.nq(rule)
+    cached = not cfg.name.startswith("c4")
+    return {"workload": f"{cfg.name}: {cfg.kind} {cfg.ncells}x{cfg.ncells} cells, p={cfg.p}, "
+                        f"{rule} rule nq={nq}, (1 residual + {cfg.k_mv} Jacobian matvecs)"
+                        + (f" x {cfg.reps}" if cfg.reps > 1 else "")
+                        + (f", alpha cycling {list(cfg.alphas)}" if len(cfg.alphas) > 1 else ""),
+            "rule": rule, "ncells": cfg.N, "p": cfg.p, "nq": nq, "k_mv": cfg.k_mv, "reps": cfg.reps,
+            "matvec": "cached point weights" if cached else "weights recomputed from psi (fused with the residual)",
+            "l2": "flushed between timed steps (256 MB write)",
+            "eqp_per_step": cfg.N * nq * nq * (1 + cfg.k_mv) * cfg.reps}
+
+
+# dram bytes per launch of the dominant kernel from one `ncu --set full` capture
+# (cold caches: ncu flushes L2 between replays), see profiles/
+NCU_TRAFFIC = {("c1", "gauss"): (26323968.0, "profiles/r01_ncu_full_c1_apply.txt")}
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
@@ -184,9 +205,7 @@ def run_reference(args, cfg, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8d)",
-        "config": {"workload": f"{cfg.name} {cfg.kind} {cfg.ncells}x{cfg.ncells} p={cfg.p} "
-                               f"{rule} nq={cfg.nq(rule)}: 1 residual + {cfg.k_mv} matvecs",
-                   "rule": rule},
+        "config": config_dict(cfg, rule),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -335,7 +354,9 @@ def main():
         roof = {"kernel": "k_warp<NT,QT,M_OBST_CACHED> (Jacobian apply from cached weights)"
                 if cfg.kind == "obstacle" else "Jacobian apply from cached weights (gradient)",
                 "bound": "tensor", "achieved": achieved, "peak": P_FP64_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / P_FP64_TFLOPS, "traffic": None,
+                "frac": achieved / P_FP64_TFLOPS,
+                "traffic": NCU_TRAFFIC.get((cfg.name, rule), (None, None))[0],
+                "traffic_source": NCU_TRAFFIC.get((cfg.name, rule), (None, "not captured for this config"))[1],
                 "peak_source": "measured FP64 DMMA peak (profiles/fp64_peaks_r01.json)",
                 "algorithmic_per_launch": {"flops": F_mv, "bytes": B_mv},
                 "avg_launch_us": t_k * 1e6}
@@ -394,14 +415,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inputs with the config's shapes and value laws, SURVEY.md §8d)",
-            "config": {"workload": f"{cfg.name}: {cfg.kind} {cfg.ncells}x{cfg.ncells} cells, p={cfg.p}, "
-                                   f"{rule} rule nq={nq}, (1 residual + {kmv} Jacobian matvecs)"
-                                   + (f" x {reps}" if reps > 1 else "")
-                                   + (f", alpha cycling {list(cfg.alphas)}" if len(cfg.alphas) > 1 else ""),
-                       "rule": rule, "ncells": cfg.N, "p": cfg.p, "nq": nq, "k_mv": kmv, "reps": reps,
-                       "matvec": "cached point weights" if cached else "weights recomputed from psi",
-                       "l2": "flushed between timed steps (256 MB write)",
-                       "eqp_per_step": eqp_step},
+            "config": config_dict(cfg, rule),
             "roofline": roof,
             "step_roofline_frac": step_frac,
             "cpu_baseline": cpu,
