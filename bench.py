@@ -230,17 +230,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if world > 1:
-            import torch.distributed as dist
-            dist.init_process_group("gloo")
+        # the reference arm is a CPU run: rank 0 alone measures and prints, the
+        # other ranks exit without work
         run_reference(args, cfg, rank, world)
         return
 
     import torch
     import torch.distributed as dist
+
+    from paper_2412_13733_b200 import dist as hdist
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    hdist.init("nccl")   # one process per GPU; weak scaling: each rank owns a config-sized slab
     from paper_2412_13733_b200 import disc as D
     from paper_2412_13733_b200.mesh import uniform_mesh_2d
     from paper_2412_13733_b200.proximal import residual
@@ -325,25 +325,19 @@ def main():
     with torch.cuda.stream(stream):
         run_steps(args.warmup, False)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        hdist.barrier(dev)
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
             evs = run_steps(args.steps, True)
             torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        hdist.barrier(dev)
         torch.cuda.synchronize()
     step_ms = [e0.elapsed_time(e2) for e0, e1, e2 in evs]
     res_ms = [e0.elapsed_time(e1) for e0, e1, e2 in evs]
     mv_ms = [e1.elapsed_time(e2) for e0, e1, e2 in evs] if cached else None
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = hdist.max_over_ranks(sum(step_ms), dev)       # slowest rank
     eqp_step = cfg.N * nq * nq * (1 + kmv) * reps
-    value = eqp_step * args.steps * world / (total_ms * 1e-3)
+    value = hdist.aggregate_throughput(eqp_step, args.steps, world, total_ms * 1e-3)
 
     # roofline of the dominant kernel
     F_res, F_mv, B_res, B_mv = algorithmic(cfg, disc.n, nq, disc.ndof_psi, disc.ndof_u)
