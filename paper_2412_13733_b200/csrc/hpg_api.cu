@@ -9,6 +9,7 @@
 
 #include "../../include/hpg_b200.h"
 #include "hpg_blocks.cuh"
+#include "hpg_blockrow.cuh"
 #include "hpg_common.cuh"
 #include "hpg_launch.cuh"
 #include "hpg_useside.cuh"
@@ -84,6 +85,7 @@ struct hpgPlan_st {
   size_t partial_len = 0;
   double* Z = nullptr;          // blocks stage-1 scratch
   double* edge = nullptr;       // [N][4m-4] residual hat contributions
+  double* PKG = nullptr;        // block-row B-operand table PK(G) [n][NT][QK][32]
   double* ubuf = nullptr;       // CTA path U-side scratch (large m)
   bool small = false;           // thread-per-element low-degree path available
   SmallTables stab;             // its tables (kernel-parameter / constant bank)
@@ -220,6 +222,21 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
       for (int g = 0; g < nq; ++g)
         G[((size_t)a * P->n + j) * P->QP + g] = T[(size_t)a * nq + g] * S[(size_t)g * P->n + j];
   if ((rc = upload(&P->G, G.data(), G.size()))) { delete P; return rc; }
+  {
+    // PK(G)[b][nt][ks][lane] = G[(b, k = 8nt + r)][h = 8(ks>>1) + 2c + (ks&1)]
+    const int QK = 2 * P->QT;
+    std::vector<double> pkg((size_t)P->n * P->NT * QK * 32, 0.0);
+    for (int b = 0; b < P->n; ++b)
+      for (int nt = 0; nt < P->NT; ++nt)
+        for (int ks = 0; ks < QK; ++ks)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int r = lane >> 2, c = lane & 3;
+            const int k = 8 * nt + r, h = 8 * (ks >> 1) + 2 * c + (ks & 1);
+            if (k < P->n && h < nq)
+              pkg[(((size_t)b * P->NT + nt) * QK + ks) * 32 + lane] = G[((size_t)b * P->n + k) * P->QP + h];
+          }
+    if ((rc = upload(&P->PKG, pkg.data(), pkg.size()))) { delete P; return rc; }
+  }
   cudaError_t e = cudaMalloc(&P->scratch_u, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
   if (e == cudaSuccess) e = cudaMalloc(&P->mu, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
   if (e == cudaSuccess) e = cudaMalloc(&P->dflag, sizeof(int) * 4);
@@ -255,7 +272,7 @@ int hpgPlanDestroy(hpgPlan P) {
   if (P == nullptr) return HPG_OK;
   cudaFree(P->Sf); cudaFree(P->Tf); cudaFree(P->hx); cudaFree(P->hy); cudaFree(P->G);
   cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
-  cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag); cudaFree(P->edge); cudaFree(P->ubuf);
+  cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag); cudaFree(P->edge); cudaFree(P->PKG); cudaFree(P->ubuf);
   delete P;
   return HPG_OK;
 }
@@ -406,12 +423,7 @@ int hpgResidualApply(hpgPlan P, double alpha, const double* psi_prev, const doub
                        stream);
 }
 
-int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {
-  if (int rc = check(P)) return rc;
-  if (!wcache || !blocks) return fail(HPG_ERR_ARG, "null pointer");
-  if (c0 < 0 || count < 0 || c0 + count > P->N) return fail(HPG_ERR_ARG, "cell range out of bounds");
-  if (count == 0) return HPG_OK;
-  cudaStream_t s = (cudaStream_t)stream;
+static int blocks_gemm(hpgPlan P, const double* wcache, double* blocks, int c0, int count, cudaStream_t s) {
   int nf = P->kind == HPG_OBSTACLE ? 1 : 3;
   int n2 = P->n * P->n;
   // stage-1 scratch sized for up to 256 MB of Z per pass
@@ -444,6 +456,60 @@ int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count
     k_gemm<1><<<g2, 256, 0, s>>>(g);
     LAUNCH_CHECK();
   }
+  return HPG_OK;
+}
+
+int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!wcache || !blocks) return fail(HPG_ERR_ARG, "null pointer");
+  if (c0 < 0 || count < 0 || c0 + count > P->N) return fail(HPG_ERR_ARG, "cell range out of bounds");
+  if (count == 0) return HPG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  BArgs B;
+  memset(&B, 0, sizeof(B));
+  B.n = P->n; B.NT = P->NT; B.QT = P->QT; B.nq = P->nq;
+  B.nf = P->kind == HPG_OBSTACLE ? 1 : 3;
+  B.ncy = P->ncy; B.cell0 = c0; B.ncell = count;
+  B.G = P->G; B.PKG = P->PKG; B.wc = wcache; B.out = blocks;
+  B.nb = (long long)P->n * P->n * (P->kind == HPG_OBSTACLE ? 1 : 2);
+  B.hx = P->hx; B.hy = P->hy;
+  B.per_warp = 1;
+  const int threads = 128;
+  const size_t zs = sizeof(double) * (size_t)P->NT * P->QT * 64;
+  const size_t pks = sizeof(double) * (size_t)P->n * P->NT * 2 * P->QT * 32;
+  const size_t so = sizeof(double) * (size_t)(8 * P->NT) * (8 * P->NT + 1);
+  const size_t smem = pks + (zs + so) * (threads / 32);
+  if (smem > ((size_t)200 << 10) || P->NT > 4) {
+    // large tiles: two-stage GEMM (Z = G W, blocks = Z G^T) through global scratch
+    return blocks_gemm(P, wcache, blocks, c0, count, s);
+  }
+  void* fn;
+  switch (P->NT) {
+    case 1: fn = (void*)k_blockrow<1>; break;
+    case 2: fn = (void*)k_blockrow<2>; break;
+    case 3: fn = (void*)k_blockrow<3>; break;
+    case 4: fn = (void*)k_blockrow<4>; break;
+    case 5: fn = (void*)k_blockrow<5>; break;
+    case 6: fn = (void*)k_blockrow<6>; break;
+    case 7: fn = (void*)k_blockrow<7>; break;
+    case 8: fn = (void*)k_blockrow<8>; break;
+    case 9: fn = (void*)k_blockrow<9>; break;
+    case 10: fn = (void*)k_blockrow<10>; break;
+    case 11: fn = (void*)k_blockrow<11>; break;
+    case 12: fn = (void*)k_blockrow<12>; break;
+    default: fn = nullptr;
+  }
+  if (fn == nullptr) return fail(HPG_ERR_UNSUPPORTED, "block-row kernel supports n <= 96");
+  if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+  const long long items = (long long)count * B.nf * P->n;
+  const long long per_cta = B.per_warp ? threads / 32 : 1;
+  long long need = (items + per_cta - 1) / per_cta;
+  long long cap = (long long)P->nsm * (occ > 0 ? occ : 1);
+  int grid = (int)(need < cap ? need : cap);
+  void* args[] = {&B};
+  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, s));
   return HPG_OK;
 }
 
