@@ -167,26 +167,23 @@ class _DeviceDisc:
             self._devbuf[tag] = b
         return b[:n]
 
+    # Host<->device transfers of the reference-facing API.  Measured on the
+    # B200 boxes (tools/xfer_bench.py, 7.4 MB): a direct pageable copy is as
+    # fast as pinned staging + host memcpy for H2D and faster end to end for
+    # D2H into a fresh array, so both go straight between the NumPy buffer and
+    # device memory (the driver pipelines its own staging).
     def h2d(self, arr, tag):
-        """Host array -> device tensor through a reusable pinned staging buffer."""
+        """Host array -> (reused) device tensor."""
         a = np.ascontiguousarray(arr, dtype=np.float64).reshape(-1)
-        pin = self._pin("in_" + tag, a.size)
-        ev = self._events.get(tag)
-        if ev is not None:
-            ev.synchronize()      # the previous async copy out of this buffer is done
-        pin.numpy()[:] = a
         dev = self._dev("in_" + tag, a.size)
-        dev.copy_(pin, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._events[tag] = ev
+        dev.copy_(torch.from_numpy(a))
         return dev
 
     def d2h(self, t, tag):
-        pin = self._pin("out_" + tag, t.numel())
-        pin.copy_(t.reshape(-1), non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return pin.numpy().copy()
+        """Device tensor -> fresh host array (the reference returns fresh arrays)."""
+        out = np.empty(t.numel())
+        torch.from_numpy(out).copy_(t.reshape(-1))
+        return out
 
     def _check_len(self, v, n, what):
         if v.numel() != n:
