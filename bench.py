@@ -393,6 +393,33 @@ def main():
                "ms_per_step": 1e3 * statistics.mean(t_e2e),
                "path": "paper_2412_13733_b200.proximal.residual + disc.assemble_D + (D @ x) x k_mv, NumPy in/out"}
 
+    # element-block assembly (reported separately): configs whose
+    # BASELINE workload includes it
+    blocks = None
+    if cfg.name in ("c0", "c2", "c3") and world == 1:
+        disc.residual_t(cfg.alphas[0], psi_prev, u, psi, b_u=b_u, b_psi=b_psi, flag=flag, wcache=True)
+        nbl = disc.plan.block_len
+        chunk = max(1, min(cfg.N, int((8 << 30) // (8 * nbl))))      # <= 8 GB of blocks per launch
+        out_blk = torch.empty((chunk, nbl), dtype=torch.float64, device=dev)
+        disc.blocks_t(out=out_blk, c0=0, count=chunk)
+        torch.cuda.synchronize()
+        eb0 = torch.cuda.Event(enable_timing=True)
+        eb1 = torch.cuda.Event(enable_timing=True)
+        eb0.record()
+        for c0 in range(0, cfg.N, chunk):
+            disc.blocks_t(out=out_blk, c0=c0, count=min(chunk, cfg.N - c0))
+        eb1.record()
+        torch.cuda.synchronize()
+        t_blk = eb0.elapsed_time(eb1) * 1e-3
+        nb_ = cfg.ncomp * disc.n * disc.n
+        nbfield = 1 if cfg.kind == "obstacle" else 3
+        F_blk = cfg.N * nbfield * (2.0 * disc.n ** 4 * nq + 2.0 * disc.n ** 2 * nq ** 2)
+        B_blk = 8.0 * cfg.N * nb_ * nb_ + 8.0 * disc.ndof_psi
+        t_lb = max(F_blk / (P_FP64_TFLOPS * 1e12), B_blk / (hbm * 1e9))
+        blocks = {"ms": t_blk * 1e3, "tflops": F_blk / t_blk / 1e12, "gbs": B_blk / t_blk / 1e9,
+                  "roofline_frac": t_lb / t_blk, "bytes": B_blk, "flops": F_blk}
+        del out_blk
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -412,6 +439,7 @@ def main():
             "config": config_dict(cfg, rule),
             "roofline": roof,
             "step_roofline_frac": step_frac,
+            "blocks": blocks,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,

@@ -252,11 +252,13 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   P->use_warp[M_GRAD_CACHED] = warp_fits(M_GRAD_CACHED, P->NT, P->QT);
   P->use_warp[M_VALUES] = 0;
   // split the Q row tiles of an element across CTAs when there are few elements
+  // (one wave: the largest divisor of QT with N * splits <= #SMs, so every
+  // split gets the same number of row tiles)
   P->splits = 1;
-  if (P->N < 2 * P->nsm) {
-    int want = (2 * P->nsm + P->N - 1) / P->N;
-    P->splits = want < P->QT ? want : P->QT;
-    if (P->splits < 1) P->splits = 1;
+  if (P->N < P->nsm) {
+    int cap = P->nsm / P->N;
+    for (int d = 1; d <= P->QT && d <= cap; ++d)
+      if (P->QT % d == 0) P->splits = d;
   }
   P->partial_len = (size_t)P->N * P->splits * 2 * P->NP * P->NP;
   int NPu = 8 * P->NTu;

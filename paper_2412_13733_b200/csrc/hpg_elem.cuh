@@ -325,6 +325,7 @@ k_cta(ElemArgs A) {
       int f = it / NT, nt = it - f * NT;
       double P[2] = {0.0, 0.0};
       const double* col = sTile + f * TILE + 8 * nt + r;
+      #pragma unroll 8
       for (int ks = 0; ks < NK; ++ks)
         dmma(P, __ldg(A.Sf + (rt * NK + ks) * 32 + lane), col[(8 * (ks >> 1) + 2 * c + (ks & 1)) * LDT]);
       *reinterpret_cast<double2*>(sP + (f * NT + nt) * 64 + 2 * lane) = make_double2(P[0], P[1]);
@@ -336,6 +337,7 @@ k_cta(ElemArgs A) {
 #pragma unroll
       for (int f = 0; f < NSYN; ++f) {
         V[f][0] = V[f][1] = 0.0;
+        #pragma unroll 8
         for (int t = 0; t < NT; ++t) {
           double2 pa = *reinterpret_cast<const double2*>(sP + (f * NT + t) * 64 + 2 * lane);
           dmma(V[f], pa.x, __ldg(A.Sf + (ht * NK + 2 * t) * 32 + lane));
@@ -353,6 +355,7 @@ k_cta(ElemArgs A) {
     for (int it = warp; it < NOUT * NT; it += CTA_WARPS) {
       int o = it / NT, bt = it - o * NT;
       double R[2] = {0.0, 0.0};
+      #pragma unroll 8
       for (int t = 0; t < QT; ++t) {
         double2 vb = *reinterpret_cast<const double2*>(sV + (o * QT + t) * 64 + 2 * lane);
         dmma(R, __ldg(A.Tf + (bt * QK + 2 * t) * 32 + lane), vb.x);
