@@ -38,8 +38,7 @@ __device__ __forceinline__ long long wc_index(int e, int QT, int rt, int ht, int
 // Final value of moment (a, b), output component o, of cell e.
 template <int MODE>
 __device__ __forceinline__ void write_moment(const ElemArgs& A, int e, int cx, int cy, int o,
-                                             int a, int b, double y, const double* sBTu = nullptr,
-                                             const double* inv = kInvOdd) {
+                                             int a, int b, double y, const double* inv = kInvOdd) {
   constexpr bool gradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
   double wa = A.hx[cx] * inv[a];
   double wb = A.hy[cy] * inv[b];
@@ -49,17 +48,11 @@ __device__ __forceinline__ void write_moment(const ElemArgs& A, int e, int cx, i
     return;
   }
   long long idx = (long long)o * A.ncomp + psi_index(A, cx, cy, a, b);
-  if (A.residual == 2) {
-    // b_psi already holds phi_moments - B^T u (obstacle) / -B^T u (gradient)
-    // from k_ucell: finish proximal.py:123 / :125 in the reference's order
+  if (A.residual) {
+    // b_psi already holds phi_mom - B^T u (obstacle) / -B^T u (gradient) from
+    // the U-side kernel: finish proximal.py:123 / :125 in the reference's order
     if constexpr (gradient) val = A.out[idx] + val;
     else val = A.out[idx] - val;
-  } else if (A.residual) {
-    // proximal.py:123 / :125
-    double btu = sBTu != nullptr ? sBTu[(o * A.n + a) * A.n + b]
-                                 : btu_value(A, gradient, o, cx, cy, a, b, wa, wb);
-    if constexpr (gradient) val = val - btu;
-    else val = (__ldg(A.phi_mom + idx) - btu) - val;
   }
   A.out[idx] = val;
 }
@@ -145,9 +138,6 @@ k_warp(ElemArgs A) {
   const int r = lane >> 2, c = lane & 3;
   double* sTile = sT + NP * QP + warp * (NIN > 0 ? NIN * TILE : 0);
   double* sInv = sT + NP * QP + WARP_CTA_WARPS * NIN * TILE;      // 1/(2k+1), k < NP
-  double* sU = sInv + NP + warp * A.usmem;
-  constexpr bool kResidual = MODE == M_OBST_RES || MODE == M_GRAD_RES;
-  constexpr bool kGradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
   for (int i = threadIdx.x; i < QP * NP; i += blockDim.x) {
     sS[i] = A.Sf[i];
     sT[i] = A.Tf[i];
@@ -171,15 +161,6 @@ k_warp(ElemArgs A) {
       }
     }
     __syncwarp();
-    const double* sBTu = nullptr;
-    if constexpr (kResidual) {
-      if (A.residual == 1) {
-        double* btu = sU + 4 * A.m * ucell_ld(A.m);
-        ucell_residual<kGradient>(A, e, cx, cy, sTile, sTile + TILE, LDT, sU, btu, lane, 32, WarpSync{});
-        sBTu = btu;
-      }
-    }
-
     double Y[NOUT][NT][NT][2];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
@@ -254,7 +235,7 @@ k_warp(ElemArgs A) {
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             int a = 8 * at + 2 * c + j, b = 8 * bt + r;
-            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j], sBTu, sInv);
+            if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j], sInv);
           }
     __syncwarp();
   }
@@ -278,15 +259,11 @@ k_cta(ElemArgs A) {
   double* sP = sTile + NIN * TILE;               // [NSYN][NT][64]
   double* sV = sP + NSYN * NT * 64;               // [NOUT][QT][64]
   double* sR = sV + NOUT * QT * 64;               // [NOUT][NT][64]
-  constexpr bool kResidual = MODE == M_OBST_RES || MODE == M_GRAD_RES;
-  constexpr bool kGradient = MODE >= M_GRAD_RES && MODE <= M_GRAD_CACHED;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
   const int e = blockIdx.x / A.splits, sp = blockIdx.x - e * A.splits;
   if (e >= A.N) return;
   const int rt0 = (sp * QT) / A.splits, rt1 = ((sp + 1) * QT) / A.splits;
-  double* sU = A.ubuf != nullptr ? A.ubuf + (long long)e * A.usmem   // U side (residual only)
-                                 : sR + NOUT * NT * 64;
   const int cx = e / A.ncy, cy = e - cx * A.ncy;
 
   for (int f = 0; f < NIN; ++f) {
@@ -302,17 +279,6 @@ k_cta(ElemArgs A) {
     }
   }
   __syncthreads();
-  const double* sBTu = nullptr;
-  if constexpr (kResidual) {
-    // U side once per element: by the CTA holding the first row-tile split
-    if (A.residual == 1 && sp == 0) {
-      double* btu = sU + 4 * A.m * ucell_ld(A.m);
-      ucell_residual<kGradient>(A, e, cx, cy, sTile, sTile + TILE, LDT, sU, btu, threadIdx.x,
-                                blockDim.x, BlockSync{});
-      sBTu = btu;
-    }
-  }
-
   const int ny = NOUT * NT * NT;
   double Y[MAXS][2];
 #pragma unroll
@@ -390,7 +356,7 @@ k_cta(ElemArgs A) {
       for (int j = 0; j < 2; ++j) {
         int a = 8 * at + 2 * c + j, b = 8 * bt + r;
         if (A.splits == 1) {
-          if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[s][j], sBTu);
+          if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[s][j]);
         } else {
           A.partial[(((long long)e * A.splits + sp) * NOUT + o) * NP * NP + a * NP + b] = Y[s][j];
         }
