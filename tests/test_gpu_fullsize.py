@@ -1,0 +1,142 @@
+"""GPU parity at BASELINE.json's full sizes against the (golden-pinned) CPU
+oracle, plus size-independent properties:
+* c1/c2/c3/c4 residual and Jacobian apply vs the oracle on the full meshes;
+* D(psi) x three ways (matrix-free from psi, from cached weights, dense blocks);
+* exact u-side couplings (B^T u, B psi, A u) on their own;
+* linearity of the Jacobian apply in x;
+* the residual's exact zero-state identity (tests/test_proximal.py:144-153)."""
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from oracle import hpg_oracle as orc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def build(cfg_name, rule="gauss", ncells=None):
+    import torch
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    from paper_2412_13733_b200.workloads import CONFIGS, config_inputs
+    cfg = CONFIGS[cfg_name]
+    nc = cfg.ncells if ncells is None else ncells
+    inp = config_inputs(cfg, ncells=nc)
+    cls = D.ObstacleDisc2D if cfg.kind == "obstacle" else D.GradientDisc2D
+    d = cls(uniform_mesh_2d(0.0, 1.0, nc, cfg.p), inp["f"], inp["phi"], rule=rule,
+            nq=cfg.Q if rule == "gauss" else None)
+    t = d.tables
+    P = orc.Problem(cfg.kind, d.xpts, d.ypts, cfg.p,
+                    SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
+    dev = {k: torch.from_numpy(np.ascontiguousarray(inp[k])).cuda() for k in ("psi", "psi_prev", "u", "x")}
+    return cfg, d, P, inp, dev
+
+
+@pytest.mark.parametrize("cfg_name,rule", [("c1", "gauss"), ("c1", "reference"), ("c2", "gauss"),
+                                           ("c3", "gauss"), ("c3", "reference"), ("c4p2", "gauss"),
+                                           ("c4p4", "reference"), ("c4p6", "gauss")])
+def test_full_size_residual_and_apply(cfg_name, rule):
+    cfg, d, P, inp, dev = build(cfg_name, rule)
+    alpha = cfg.alphas[-1]
+    phi_vals = P.sample(inp["phi"])
+    f_load = P.load_vector(P.sample(1.0))
+    assert orc.rel_err(d.f_load, f_load) < TOL
+    if cfg.kind == "obstacle":
+        phi_mom = P.data_moments(phi_vals)
+        assert orc.rel_err(d.phi_moments, phi_mom) < TOL
+        rb_u, rb_psi, rcl = P.residual(alpha, inp["psi_prev"], inp["u"], inp["psi"], f_load,
+                                       phi_moments=phi_mom)
+        ry = P.obstacle_apply_D(inp["psi"], inp["x"])
+    else:
+        rb_u, rb_psi, rcl = P.residual(alpha, inp["psi_prev"], inp["u"], inp["psi"], f_load,
+                                       phi_vals=phi_vals)
+        ry = P.gradient_apply_D(inp["psi"], inp["x"], phi_vals)
+    b_u, b_psi, flag = d.residual_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
+    assert orc.rel_err(b_u.cpu().numpy(), rb_u) < TOL
+    assert orc.rel_err(b_psi.cpu().numpy(), rb_psi) < TOL
+    if cfg.kind == "obstacle":
+        assert bool(flag.item()) == rcl
+    y_cached = d.apply_cached_t(dev["x"]).cpu().numpy()
+    y_psi = d.apply_D_t(dev["psi"], dev["x"]).cpu().numpy()
+    assert orc.rel_err(y_cached, ry) < TOL
+    assert orc.rel_err(y_psi, ry) < TOL
+    b_u2, b_psi2, y2, _ = d.residual_apply_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], dev["x"])
+    assert orc.rel_err(b_psi2.cpu().numpy(), rb_psi) < TOL
+    assert orc.rel_err(y2.cpu().numpy(), ry) < TOL
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c4p4"])
+def test_u_side_couplings(cfg_name):
+    cfg, d, P, inp, dev = build(cfg_name, ncells=8 if cfg_name != "c4p4" else 32)
+    assert orc.rel_err(d.BT_u_t(dev["u"]).cpu().numpy(), P.BT_u(inp["u"])) < TOL
+    assert orc.rel_err(d.B_psi_t(dev["psi"]).cpu().numpy(), P.B_psi(inp["psi"])) < TOL
+    assert orc.rel_err(d.A_u_t(dev["u"]).cpu().numpy(), P.A_u(inp["u"])) < TOL
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3"])
+def test_blocks_three_ways(cfg_name):
+    """dense-block matvec == cached matrix-free apply == apply from psi."""
+    import torch
+    cfg, d, P, inp, dev = build(cfg_name, ncells=4 if cfg_name != "c3" else 2)
+    D = d.assemble_D_t(dev["psi"])
+    y1 = D.matvec_t(dev["x"]).cpu().numpy()
+    y2 = D.matvec_blocks_t(dev["x"]).cpu().numpy()
+    y3 = d.apply_D_t(dev["psi"], dev["x"]).cpu().numpy()
+    assert orc.rel_err(y2, y1) < TOL
+    assert orc.rel_err(y3, y1) < TOL
+    # selected cells against the oracle's einsum blocks
+    if cfg.kind == "obstacle":
+        ref, _ = P.obstacle_blocks(inp["psi"])
+    else:
+        ref = P.gradient_blocks(inp["psi"], P.sample(inp["phi"]))
+    got = D.blocks_t().cpu().numpy()
+    assert orc.rel_err(got, ref) < TOL
+    del torch
+
+
+def test_apply_is_linear_in_x():
+    import torch
+    cfg, d, P, inp, dev = build("c1", ncells=16)
+    x2 = torch.from_numpy(np.random.default_rng(7).standard_normal(d.ndof_psi)).cuda()
+    d.residual_t(1.0, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
+    a = d.apply_cached_t(dev["x"])
+    b = d.apply_cached_t(x2)
+    ab = d.apply_cached_t(2.5 * dev["x"] - 0.5 * x2)
+    diff = (ab - (2.5 * a - 0.5 * b)).abs().max().item()
+    assert diff / a.abs().max().item() < 1e-13
+
+
+def test_residual_zero_state():
+    """b_u == 0 exactly and b_psi == phi_moments - exp_moments(0) at the zero state
+    with f = 0 (reference tests/test_proximal.py:144-153, here in 2D)."""
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    from paper_2412_13733_b200.proximal import residual
+    d = D.ObstacleDisc2D(uniform_mesh_2d(0.0, 1.0, 4, 3), 0.0, 2.0)
+    z_psi, z_u = np.zeros(d.ndof_psi), np.zeros(d.ndof_u)
+    b_u, b_psi, cl = residual(d, 0.5, z_psi, z_u, z_psi)
+    assert not cl
+    assert np.abs(b_u).max() == 0.0
+    em, _ = d.exp_moments(z_psi)
+    np.testing.assert_allclose(b_psi, d.phi_moments - em, atol=1e-15)
+
+
+def test_cellwise_data_and_moments_from_values():
+    """phi_mode='cellwise' broadcast and moments_from_values (assembly.py:308-317,528-533)."""
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    phi = lambda x, y: np.sin(x) * (1 + y)
+    d = D.ObstacleDisc2D(uniform_mesh_2d(0.0, 1.0, 3, 4), 1.0, phi, phi_mode="cellwise")
+    t = d.tables
+    P = orc.Problem("obstacle", d.xpts, d.ypts, 4,
+                    SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
+    mx = 0.5 * (d.xpts[:-1] + d.xpts[1:])
+    my = 0.5 * (d.ypts[:-1] + d.ypts[1:])
+    vals = np.broadcast_to(phi(mx[:, None], my[None, :])[:, :, None, None],
+                           (3, 3, t.nq, t.nq)).copy()
+    assert orc.rel_err(d.phi_moments, P.data_moments(vals)) < TOL
+    grids = d.quad_grids()
+    samples = [phi(*np.meshgrid(gx, gy, indexing="ij")) for gx, gy in grids]
+    assert orc.rel_err(d.moments_from_values(samples), P.data_moments(P.sample(phi))) < TOL
