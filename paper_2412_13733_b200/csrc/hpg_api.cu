@@ -3,6 +3,7 @@
 // device), path selection and kernel launches.  No allocation in the hot
 // entry points: every workspace is sized at plan creation.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -366,6 +367,9 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
   if (usmall_available(P->p, P->kind == HPG_GRADIENT)) {
     // (1) U side, low degree: thread per cell, generated straight-line code
     if ((rc = run_usmall(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
+  } else if (P->kind == HPG_OBSTACLE && upass_available(P->p) && getenv("HPG_UPASS_OFF") == nullptr) {
+    // (1) U side, mid degree: warp per cell, generated separable passes
+    if ((rc = run_upass(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
   } else {
     // (1) U side (thread per cell-local entry): b_psi <- phi_mom - B^T u
     //     (obstacle) | -B^T u (gradient); b_u on owned dofs + edge scratch
