@@ -246,7 +246,7 @@ k_warp(ElemArgs A) {
 // the same four contractions, warps splitting tiles, stage results passed
 // through shared memory in C-fragment order (read back with LDS.128 by the
 // same lane).  Used for large n (config 3) and as the general path.
-template <int MODE, int MAXS>
+template <int MODE, int MAXS, int CTA_WARPS>
 __global__ void __launch_bounds__(32 * CTA_WARPS, 1)
 k_cta(ElemArgs A) {
   using TR = ModeTraits<MODE>;

@@ -37,21 +37,20 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_warp launch", e);
 }
 
-template <int MODE, int MAXS>
+template <int MODE, int MAXS, int W>
 int launch_cta_t(ElemArgs A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
   const int NP = 8 * A.NT;
   size_t smem = sizeof(double) * ((size_t)TR::NIN * NP * (NP + 2) +
-                                  (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64 +
-                                  (A.ubuf != nullptr ? 0 : (size_t)A.usmem));
+                                  (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64);
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "element tile too large for shared memory");
   static int attr = 0;
   if ((int)smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cta<MODE, MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_cta)", e);
     attr = (int)smem;
   }
-  k_cta<MODE, MAXS><<<A.N * A.splits, 32 * CTA_WARPS, smem, s>>>(A);
+  k_cta<MODE, MAXS, W><<<A.N * A.splits, 32 * W, smem, s>>>(A);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_cta launch", e);
   if (A.splits > 1) {
@@ -63,14 +62,22 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
   return 0;
 }
 
+// few elements split across CTAs (config 3): 16 warps per CTA for latency
+// hiding; many elements (config 2): 8 warps per CTA, more CTAs per SM
+template <int MODE, int W>
+int launch_cta_w(ElemArgs A, cudaStream_t s) {
+  using TR = ModeTraits<MODE>;
+  int slots = (TR::NOUT * A.NT * A.NT + W - 1) / W;
+  if (slots <= 4) return launch_cta_t<MODE, 4, W>(A, s);
+  if (slots <= 16) return launch_cta_t<MODE, 16, W>(A, s);
+  if (slots <= 32) return launch_cta_t<MODE, 32, W>(A, s);
+  return set_error_msg(HPG_ERR_UNSUPPORTED, "tile side too large");
+}
+
 template <int MODE>
 int launch_cta(ElemArgs A, cudaStream_t s) {
-  using TR = ModeTraits<MODE>;
-  int slots = (TR::NOUT * A.NT * A.NT + CTA_WARPS - 1) / CTA_WARPS;
-  if (slots <= 4) return launch_cta_t<MODE, 4>(A, s);
-  if (slots <= 16) return launch_cta_t<MODE, 16>(A, s);
-  if (slots <= 32) return launch_cta_t<MODE, 32>(A, s);
-  return set_error_msg(HPG_ERR_UNSUPPORTED, "tile side too large");
+  if (A.splits > 1) return launch_cta_w<MODE, 16>(A, s);
+  return launch_cta_w<MODE, 8>(A, s);
 }
 
 }  // namespace
