@@ -484,7 +484,13 @@ int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count
   const size_t zs = sizeof(double) * (size_t)P->NT * P->QT * 64;
   const size_t pks = sizeof(double) * (size_t)P->n * P->NT * 2 * P->QT * 32;
   const size_t so = sizeof(double) * (size_t)(8 * P->NT) * (8 * P->NT + 1);
-  const size_t smem = pks + (zs + so) * (threads / 32);
+  size_t smem = pks + (zs + so) * (threads / 32);
+  B.pk_smem = 1;
+  if (smem > ((size_t)200 << 10) && P->NT <= 4) {
+    // PK(G) too large to stage: read it from L2 (shared by every cell)
+    B.pk_smem = 0;
+    smem = (zs + so) * (threads / 32);
+  }
   if (smem > ((size_t)200 << 10) || P->NT > 4) {
     // large tiles: two-stage GEMM (Z = G W, blocks = Z G^T) through global scratch
     return blocks_gemm(P, wcache, blocks, c0, count, s);

@@ -21,6 +21,7 @@ struct BArgs {
   int n, NT, QT, nq, nf, ncy;
   int cell0, ncell;        // cells [cell0, cell0 + ncell)
   int per_warp;            // 1: one warp per item; 0: one CTA per item
+  int pk_smem;             // 1: PK(G) staged in shared memory; 0: read from L2
   const double* G;         // [n*n][QP]
   const double* PKG;       // [n][NT][2*QT][32]
   const double* wc;        // weight cache (C-fragment order), NW = nf
@@ -49,8 +50,9 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
   const long long groups_total = (long long)gridDim.x * (B.per_warp ? nwarps : 1);
   // the B-operand table PK(G) staged once per CTA (shared by all items)
   double* sPK = smem;
-  const long long pk_len = (long long)n * NT * QK * 32;
+  const long long pk_len = B.pk_smem ? (long long)n * NT * QK * 32 : 0;
   for (long long i = threadIdx.x; i < pk_len; i += blockDim.x) sPK[i] = __ldg(B.PKG + i);
+  const double* PKb = B.pk_smem ? sPK : B.PKG;
   double* sZ = smem + pk_len + (size_t)gid * zsize;
   // per-group output staging tile (NP x NP), written back as a contiguous block row
   const int NP = 8 * NT, LDO = NP + 1;
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
 #pragma unroll
           for (int ci = 0; ci < NC; ++ci) {
             const int nt = nt0 + ci * gw;
-            const double* pk = sPK + (((long long)b * NT + (nt < NT ? nt : 0)) * QK + 2 * ht) * 32 + lane;
+            const double* pk = PKb + (((long long)b * NT + (nt < NT ? nt : 0)) * QK + 2 * ht) * 32 + lane;
             bf[ci][0] = nt < NT ? pk[0] : 0.0;
             bf[ci][1] = nt < NT ? pk[32] : 0.0;
           }
