@@ -16,7 +16,9 @@
  *    row-major array; gradient vectors stack [psi_x ; psi_y]
  *    (assembly.py:744-745).
  *  - u-side vectors are interior U coefficients (spaces.py:188-189): a
- *    (nix x niy) row-major array, nix = ncx*p - 1.
+ *    (nix x niy) row-major array, nix = ncx*p - 1.  When the mesh has no
+ *    interior U dof (gradient p = 1 on one cell row), u-side pointers may be
+ *    NULL.
  *  - Cell order (blocks, point samples) is (cx, cy) cx-major
  *    (assembly.py:482).  Point samples are (ncells, nq, nq) row-major.
  *  - Every call returns 0 on success, a nonzero HPG_ERR_* code otherwise;
@@ -113,6 +115,38 @@ int hpgAu(hpgPlan plan, const double* u, double* out, void* stream);
 int hpgMomentsFromValues(hpgPlan plan, const double* vals, double* out,
                          void* stream);
 int hpgLoadVector(hpgPlan plan, const double* vals, double* out, void* stream);
+
+/* Per-cell Schur preconditioner.
+ *
+ * hpgPrecondPrepare replaces ObstacleDisc2D.schur_hat_triple
+ * (assembly.py:577-595): builds, per distinct (hx, hy) width key, the triple
+ * Bhat^T Ahat^{-1} Bhat from the reference-cell eigen-factors of
+ * Ahat = Kx(x)My + Mx(x)Ky: Zhat (n x n, row-major) = Ghat^T Khat^{-1/2} V and
+ * lam_hat (n) with Khat^{-1/2} Mhat Khat^{-1/2} = V diag(lam_hat) V^T
+ * (tables.py: schur_triple_factors).  No-op for gradient plans.
+ *
+ * hpgPrecondBlocks: in place, D blocks -> precond_blocks(D, alpha, beta)
+ * (assembly.py:597-603 obstacle, :851-860 gradient) for cells [c0, c0+count).
+ * hpgLUFactor: batched LU with partial pivoting, in place (scipy lu_factor,
+ * linalg.py:249), ipiv[count][nb] 0-based like lu_factor's piv; `info`
+ * (device int, may be NULL) is OR-ed with 1 if an entry is non-finite (scipy's
+ * check_finite raises ValueError there) and 2 on an exactly zero pivot
+ * (LAPACK info > 0; scipy warns).
+ * hpgPrecondFactor: both, fused (blocks hold D on entry, LU of P on exit).
+ * hpgLUSolve: CellBlockPreconditioner.apply (linalg.py:253-257):
+ * y[idx_e] = lu_solve(LU_e, x[idx_e]) for every cell.
+ * hpgLUMaxBlock: largest block side the per-CTA factorisation supports. */
+int hpgPrecondPrepare(hpgPlan plan, const double* Zhat, const double* lam_hat,
+                      void* stream);
+int hpgPrecondBlocks(hpgPlan plan, double* blocks, double alpha, double beta,
+                     int c0, int count, void* stream);
+int hpgLUFactor(hpgPlan plan, double* blocks, int* ipiv, int count,
+                int* info, void* stream);
+int hpgPrecondFactor(hpgPlan plan, double* blocks, int* ipiv, double alpha,
+                     double beta, int c0, int count, int* info, void* stream);
+int hpgLUSolve(hpgPlan plan, const double* lu, const int* ipiv,
+               const double* x, double* y, void* stream);
+int hpgLUMaxBlock(void);
 
 const char* hpgLastError(void);
 int hpgVersion(void);

@@ -352,6 +352,70 @@ def blocks_matvec(blocks, indices, n, x):
     return out
 
 
+# ---------------------------------------------------------------------------
+# per-cell Schur preconditioner
+
+def spectral_1d(n, h):
+    """Per-cell spectral Gram, stiffness diagonal and mass (``assembly.py:128-170``)."""
+    g = np.zeros((n, n))
+    m = np.zeros((n, n))
+    k = 4.0 * (2.0 * np.arange(n) + 3.0) / h
+    for a in range(n):
+        g[a, a] = h / (2 * a + 1)
+        m[a, a] = h * (1.0 / (2 * a + 1) + 1.0 / (2 * a + 5))
+        if a + 2 < n:
+            g[a, a + 2] = -h / (2 * a + 5)
+            v = -h / (2 * a + 5)
+            m[a, a + 2] = v
+            m[a + 2, a] = v
+    return g, k, m
+
+
+def schur_hat_triple(n, hx, hy):
+    """``ObstacleDisc2D.schur_hat_triple`` (``assembly.py:577-595``), dense as the reference."""
+    gx, kx, mx = spectral_1d(n, hx)
+    gy, ky, my = spectral_1d(n, hy)
+    Ahat = np.kron(np.diag(kx), my) + np.kron(mx, np.diag(ky))
+    Bhat = np.kron(gx, gy)
+    return Bhat.T @ np.linalg.solve(Ahat, Bhat)
+
+
+def precond_blocks(prob, blocks, alpha, beta):
+    """``precond_blocks`` (obstacle ``assembly.py:597-603``, gradient ``:851-860``)."""
+    n = prob.n
+    out = []
+    cache = {}
+    for i, (cx, cy) in enumerate((cx, cy) for cx in range(prob.ncx) for cy in range(prob.ncy)):
+        hx, hy = prob.hx[cx], prob.hy[cy]
+        if prob.kind == "obstacle":
+            key = (round(hx, 15), round(hy, 15))
+            if key not in cache:
+                cache[key] = schur_hat_triple(n, hx, hy)
+            blk = -blocks[i] - cache[key] / alpha
+            mass = np.kron(hx / (2.0 * np.arange(n) + 1.0), hy / (2.0 * np.arange(n) + 1.0))
+            blk[np.diag_indices_from(blk)] -= beta * mass
+        else:
+            blk = -blocks[i].copy()
+            if beta:
+                _, kx, mx = spectral_1d(n, hx)
+                _, ky, my = spectral_1d(n, hy)
+                E = np.kron(np.diag(kx), my) + np.kron(mx, np.diag(ky))
+                m2 = n * n
+                blk[:m2, :m2] -= beta * E
+                blk[m2:, m2:] -= beta * E
+        out.append(blk)
+    return out
+
+
+def lu_precond_apply(blocks, indices, n, x):
+    """``CellBlockPreconditioner.apply`` (``linalg.py:246-257``): LAPACK getrf/getrs per cell."""
+    import scipy.linalg as sla
+    out = np.zeros(n)
+    for blk, idx in zip(blocks, indices):
+        out[idx] = sla.lu_solve(sla.lu_factor(blk), x[idx])
+    return out
+
+
 def rel_err(a, b):
     """Global max-norm relative error (SURVEY.md §8c parity metric)."""
     a = np.asarray(a, dtype=float)

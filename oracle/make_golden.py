@@ -26,7 +26,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 
-from hpgalerkin import proximal                                   # noqa: E402
+from hpgalerkin import linalg, proximal                           # noqa: E402
 from hpgalerkin.assembly import (GradientDisc2D, ObstacleDisc2D,   # noqa: E402
                                  _eval_data)
 from hpgalerkin.mesh import Mesh1D, TensorMesh2D, uniform_mesh_2d  # noqa: E402
@@ -35,6 +35,7 @@ from paper_2412_13733_b200 import tables as tb                     # noqa: E402
 from paper_2412_13733_b200.workloads import (make_inputs, phi_bilinear,  # noqa: E402
                                              phi_sin)
 
+PREC_BETA = 0.25     # large enough that the E_beta term shows in the parity checks
 OUT = os.path.join(os.path.dirname(__file__), "..", "tests", "golden")
 
 
@@ -101,12 +102,21 @@ def case(name, kind, xpts, ypts, p, rule, Q=None, alpha=1.0, phi=phi_sin,
     out["Dx"] = D @ x
     out["D_clamped"] = bool(getattr(D, "clamped", False))
     blocks = np.stack(D.blocks)
+    # per-cell Schur preconditioner (linalg.py:262-264) at PREC_BETA
+    pb = np.stack(disc.precond_blocks(D, alpha, PREC_BETA))
+    out["prec_beta"] = PREC_BETA
+    try:
+        out["precond_apply"] = linalg.schur_preconditioner(disc, D, alpha, PREC_BETA).apply(x)
+    except ValueError:          # scipy lu_factor rejects non-finite blocks
+        out["precond_error"] = True
     if block_rows is None:
         out["blocks"] = blocks
+        out["precond_blocks"] = pb
     else:
         rows = np.asarray(block_rows)
         out["block_rows"] = rows
         out["blocks_sel"] = blocks[:, rows, :]
+        out["precond_sel"] = pb[:, rows, :]
     path = os.path.join(OUT, f"{name}.npz")
     np.savez_compressed(path, **out)
     print(f"{name}: {os.path.getsize(path) / 1e6:.2f} MB  ndof_psi={psi.size} "

@@ -13,6 +13,7 @@
 #include "hpg_blockrow.cuh"
 #include "hpg_common.cuh"
 #include "hpg_launch.cuh"
+#include "hpg_precond.cuh"
 #include "hpg_useside.cuh"
 #include "hpg_small.cuh"
 #include "hpg_ucell.cuh"
@@ -90,6 +91,12 @@ struct hpgPlan_st {
   double* ubuf = nullptr;       // CTA path U-side scratch (large m)
   bool small = false;           // thread-per-element low-degree path available
   SmallTables stab;             // its tables (kernel-parameter / constant bank)
+
+  // per-cell Schur preconditioner: hat triples per width key (obstacle)
+  std::vector<double> hxh, hyh;  // host copies of the cell widths
+  double* tri = nullptr;         // [nkeys][n2][n2]
+  int* cell_key = nullptr;       // [N]
+  int nkeys = 0;
 
   int zcells = 0;
   int* dflag = nullptr;
@@ -200,6 +207,8 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   if ((rc = upload(&P->Tf, tf.data(), tf.size()))) { delete P; return rc; }
   if ((rc = upload(&P->hx, hx, ncx))) { delete P; return rc; }
   if ((rc = upload(&P->hy, hy, ncy))) { delete P; return rc; }
+  P->hxh.assign(hx, hx + ncx);
+  P->hyh.assign(hy, hy + ncy);
   // u side (load_vector): analysis with Tu, tile side m
   P->NTu = (P->m + 7) / 8;
   std::vector<double> tuf = pk_table(Tu, P->m, nq, P->NTu, P->QP);
@@ -276,6 +285,7 @@ int hpgPlanDestroy(hpgPlan P) {
   cudaFree(P->Sf); cudaFree(P->Tf); cudaFree(P->hx); cudaFree(P->hy); cudaFree(P->G);
   cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
   cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag); cudaFree(P->edge); cudaFree(P->PKG); cudaFree(P->ubuf);
+  cudaFree(P->tri); cudaFree(P->cell_key);
   delete P;
   return HPG_OK;
 }
@@ -352,7 +362,9 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
                          double* b_psi, int* clamped, double* wcache, const double* x, double* y,
                          void* stream) {
   if (int rc = check(P)) return rc;
-  if (!psi_prev || !u || !psi || !phi || !f_load || !b_u || !b_psi) return fail(HPG_ERR_ARG, "null pointer");
+  // u-side arrays are empty (and may be NULL) when the mesh has no interior U dofs
+  const bool uok = P->ndof_u == 0 || (u && f_load && b_u);
+  if (!psi_prev || !psi || !phi || !b_psi || !uok) return fail(HPG_ERR_ARG, "null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   ElemArgs A = base_args(P);
   A.in0 = psi; A.out = b_psi; A.wc_out = wcache; A.residual = 1; A.u = u;
@@ -541,7 +553,7 @@ int hpgBlocksMatvec(hpgPlan P, const double* blocks, const double* x, double* y,
 
 int hpgBTu(hpgPlan P, const double* u, double* out, void* stream) {
   if (int rc = check(P)) return rc;
-  if (!u || !out) return fail(HPG_ERR_ARG, "null pointer");
+  if ((!u && P->ndof_u > 0) || !out) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
   A.u = u; A.out = out;
   long long total = P->ndof_psi;
@@ -552,6 +564,7 @@ int hpgBTu(hpgPlan P, const double* u, double* out, void* stream) {
 
 int hpgBPsi(hpgPlan P, const double* psi, double* out, void* stream) {
   if (int rc = check(P)) return rc;
+  if (P->ndof_u == 0) return HPG_OK;
   if (!psi || !out) return fail(HPG_ERR_ARG, "null pointer");
   UArgs U = base_uargs(P);
   U.psi_a = psi; U.out = out;
@@ -560,6 +573,7 @@ int hpgBPsi(hpgPlan P, const double* psi, double* out, void* stream) {
 
 int hpgAu(hpgPlan P, const double* u, double* out, void* stream) {
   if (int rc = check(P)) return rc;
+  if (P->ndof_u == 0) return HPG_OK;
   if (!u || !out) return fail(HPG_ERR_ARG, "null pointer");
   UArgs U = base_uargs(P);
   U.u = u; U.ca = 1.0; U.out = out;
@@ -577,6 +591,7 @@ int hpgMomentsFromValues(hpgPlan P, const double* vals, double* out, void* strea
 
 int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
   if (int rc = check(P)) return rc;
+  if (P->ndof_u == 0) return HPG_OK;
   if (!vals || !out) return fail(HPG_ERR_ARG, "null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   // U-side moments Mu = wu (x) wu * (Tu F Tu^T) as x-major m-tiles
@@ -592,5 +607,104 @@ int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
   U.mu = P->mu; U.out = out;
   return run_ulocal(P, U, s);
 }
+
+// ---------------------------------------------------------------------------
+// Per-cell Schur preconditioner (assembly.py:577-603, 851-860; linalg.py:246-266)
+
+int hpgPrecondPrepare(hpgPlan P, const double* Zhat, const double* lam_hat, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (P->kind != HPG_OBSTACLE) return HPG_OK;   // the gradient blocks need no triple
+  if (!Zhat || !lam_hat) return fail(HPG_ERR_ARG, "null triple factors");
+  cudaStream_t s = (cudaStream_t)stream;
+  // width keys as the reference's _triple_cache (widths rounded to 15 digits,
+  // first cell of each key supplies the widths)
+  std::vector<long long> kx, ky;
+  std::vector<double> khx, khy;
+  std::vector<int> key(P->N);
+  for (int cx = 0; cx < P->ncx; ++cx)
+    for (int cy = 0; cy < P->ncy; ++cy) {
+      const long long a = llround(P->hxh[cx] * 1e15), b = llround(P->hyh[cy] * 1e15);
+      int k = -1;
+      for (size_t i = 0; i < kx.size(); ++i)
+        if (kx[i] == a && ky[i] == b) { k = (int)i; break; }
+      if (k < 0) {
+        k = (int)kx.size();
+        kx.push_back(a); ky.push_back(b);
+        khx.push_back(P->hxh[cx]); khy.push_back(P->hyh[cy]);
+      }
+      key[cx * P->ncy + cy] = k;
+    }
+  const int n = P->n, n2 = n * n, nk = (int)kx.size();
+  cudaFree(P->tri); P->tri = nullptr;
+  cudaFree(P->cell_key); P->cell_key = nullptr;
+  P->nkeys = 0;
+  CUDA_TRY(cudaMalloc(&P->tri, sizeof(double) * (size_t)nk * n2 * n2 + 16));
+  int rc;
+  if ((rc = upload(&P->cell_key, key.data(), key.size()))) return rc;
+  double *dZ = nullptr, *dl = nullptr, *dkx = nullptr, *dky = nullptr;
+  if ((rc = upload(&dZ, Zhat, (size_t)n2))) return rc;
+  if ((rc = upload(&dl, lam_hat, (size_t)n))) return rc;
+  if ((rc = upload(&dkx, khx.data(), khx.size()))) return rc;
+  if ((rc = upload(&dky, khy.data(), khy.size()))) return rc;
+  rc = launch_triple(dZ, dl, n, dkx, dky, nk, P->tri, s);
+  cudaStreamSynchronize(s);
+  cudaFree(dZ); cudaFree(dl); cudaFree(dkx); cudaFree(dky);
+  if (rc) return rc;
+  P->nkeys = nk;
+  return HPG_OK;
+}
+
+static int prec_args(hpgPlan P, double* blocks, int* ipiv, int* info, double alpha, double beta, int c0,
+                     int count, int transform, PrecArgs* A) {
+  if (!blocks) return fail(HPG_ERR_ARG, "null pointer");
+  if (c0 < 0 || count < 0 || c0 + count > P->N) return fail(HPG_ERR_ARG, "cell range out of bounds");
+  if (transform && P->kind == HPG_OBSTACLE && P->nkeys == 0)
+    return fail(HPG_ERR_ARG, "hpgPrecondPrepare has not been called on this plan");
+  memset(A, 0, sizeof(*A));
+  A->kind = P->kind; A->n = P->n; A->n2 = P->n * P->n;
+  A->nb = A->n2 * (P->kind == HPG_OBSTACLE ? 1 : 2);
+  A->ncy = P->ncy; A->cell0 = c0; A->count = count; A->transform = transform;
+  A->alpha = alpha; A->beta = beta;
+  A->hx = P->hx; A->hy = P->hy; A->tri = P->tri; A->key = P->cell_key;
+  A->M = blocks; A->ipiv = ipiv; A->info = info;
+  return HPG_OK;
+}
+
+int hpgPrecondBlocks(hpgPlan P, double* blocks, double alpha, double beta, int c0, int count, void* stream) {
+  if (int rc = check(P)) return rc;
+  PrecArgs A;
+  if (int rc = prec_args(P, blocks, nullptr, nullptr, alpha, beta, c0, count, 1, &A)) return rc;
+  if (count == 0) return HPG_OK;
+  return launch_precond_transform(A, (cudaStream_t)stream);
+}
+
+int hpgLUFactor(hpgPlan P, double* blocks, int* ipiv, int count, int* info, void* stream) {
+  if (int rc = check(P)) return rc;
+  PrecArgs A;
+  if (int rc = prec_args(P, blocks, ipiv, info, 1.0, 0.0, 0, count, 0, &A)) return rc;
+  if (!ipiv) return fail(HPG_ERR_ARG, "null pivot array");
+  if (count == 0) return HPG_OK;
+  return launch_lu(A, P->nsm, (cudaStream_t)stream);
+}
+
+int hpgPrecondFactor(hpgPlan P, double* blocks, int* ipiv, double alpha, double beta, int c0, int count,
+                     int* info, void* stream) {
+  if (int rc = check(P)) return rc;
+  PrecArgs A;
+  if (int rc = prec_args(P, blocks, ipiv, info, alpha, beta, c0, count, 1, &A)) return rc;
+  if (!ipiv) return fail(HPG_ERR_ARG, "null pivot array");
+  if (count == 0) return HPG_OK;
+  return launch_lu(A, P->nsm, (cudaStream_t)stream);
+}
+
+int hpgLUSolve(hpgPlan P, const double* lu, const int* ipiv, const double* x, double* y, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!lu || !ipiv || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  ElemArgs E = base_args(P);
+  const int nb = P->n * P->n * (P->kind == HPG_OBSTACLE ? 1 : 2);
+  return launch_lu_solve(E, lu, ipiv, nb, x, y, (cudaStream_t)stream);
+}
+
+int hpgLUMaxBlock(void) { return lu_max_nb(); }
 
 }  // extern "C"

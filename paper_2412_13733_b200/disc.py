@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .tables import Tables
+from .tables import Tables, schur_triple_factors
 
 F64 = torch.float64
 
@@ -281,6 +281,46 @@ class _DeviceDisc:
         clamped = self._weights_t(psi_t)
         return DeviceCellBlockMatrix(self, self._wcache.clone(), clamped)
 
+    # ------------------------------------------------ per-cell Schur preconditioner
+    def _precond_ready(self):
+        """Hat triples per width key on the device (``schur_hat_triple``, assembly.py:577-595)."""
+        if self.kind == "obstacle" and not getattr(self, "_triples_ready", False):
+            z, lam = schur_triple_factors(self.n)
+            _lib.call("hpgPrecondPrepare", self.plan.handle, z.ctypes.data_as(ctypes.c_void_p),
+                      lam.ctypes.data_as(ctypes.c_void_p), _stream())
+            self._triples_ready = True
+
+    def _blocks_of(self, D):
+        """Fresh device copy of D's element blocks (device-backed or host CellBlockMatrix)."""
+        nb = self.n * self.n * self.ncomp
+        if isinstance(D, DeviceCellBlockMatrix):
+            return self.blocks_t(wcache=D._w).view(-1, nb, nb)
+        arr = np.ascontiguousarray(np.stack(D.blocks), dtype=np.float64)
+        if arr.shape != (self.plan.ncells, nb, nb):
+            raise ValueError("D.blocks has the wrong shape")
+        return torch.from_numpy(arr).to(self.device)
+
+    def precond_blocks_t(self, D, alpha, beta):
+        """Device blocks (ncells, nb, nb) of ``precond_blocks(D, alpha, beta)``."""
+        if beta < 0:
+            raise ValueError("beta must be >= 0")
+        self._precond_ready()
+        out = self._blocks_of(D)
+        _lib.call("hpgPrecondBlocks", self.plan.handle, _vp(out), float(alpha), float(beta), 0,
+                  self.plan.ncells, _stream())
+        return out
+
+    def precond_blocks(self, D, alpha, beta):
+        """Dense blocks of -(D + E_beta + Bhat^T Ahat_alpha^{-1} Bhat) (obstacle,
+        ``assembly.py:597-603``) or -(D + E_beta) (gradient, ``:851-860``), one
+        host array per cell in ``cell_ids`` order."""
+        arr = self.precond_blocks_t(D, alpha, beta).cpu().numpy()
+        return [arr[i] for i in range(arr.shape[0])]
+
+    def schur_preconditioner(self, D, alpha, beta):
+        """``linalg.schur_preconditioner`` (linalg.py:262-264) with the per-cell LU on the GPU."""
+        return DeviceCellBlockPreconditioner.from_operator(self, D, alpha, beta)
+
     def _residual_t(self, alpha, psi_prev_t, u_t, psi_t, phi_t, b_u=None, b_psi=None, wcache=None,
                     flag=None):
         for v, n, what in ((psi_prev_t, self.ndof_psi, "psi_prev"), (u_t, self.ndof_u, "u"),
@@ -516,3 +556,92 @@ class DeviceCellBlockMatrix:
 
     def __matmul__(self, x):
         return self.matvec(x)
+
+
+class DeviceCellBlockPreconditioner:
+    """``CellBlockPreconditioner`` (``linalg.py:246-260``) with the factors on the GPU.
+
+    The per-cell blocks are LU-factorised with partial pivoting in place on the
+    device (``hpgLUFactor`` / the fused ``hpgPrecondFactor``) and ``apply``
+    runs the per-cell triangular solves on the global psi vector
+    (``hpgLUSolve``).  ``factors`` gives scipy ``lu_factor``-style
+    ``(lu, piv)`` host pairs on demand.
+    """
+
+    def __init__(self, disc, lu_t, piv_t, info_t=None, check=True):
+        self.disc = disc
+        self.lu_t = lu_t
+        self.piv_t = piv_t
+        self.info_t = info_t
+        self.n = disc.ndof_psi
+        self._factors = None
+        if check and info_t is not None:
+            self.check()
+
+    def check(self):
+        """scipy ``lu_factor`` semantics: ValueError on non-finite blocks, a
+        warning on an exactly singular block (LAPACK info > 0)."""
+        info = int(self.info_t.item())
+        if info & 1:
+            raise ValueError("array must not contain infs or NaNs")
+        if info & 2:
+            import warnings
+            warnings.warn("a per-cell preconditioner block is exactly singular", RuntimeWarning)
+
+    @classmethod
+    def from_operator(cls, disc, D, alpha, beta):
+        """Factor ``disc.precond_blocks(D, alpha, beta)`` without materialising them."""
+        if beta < 0:
+            raise ValueError("beta must be >= 0")
+        disc._precond_ready()
+        lu = disc._blocks_of(D)
+        piv = torch.empty(lu.shape[:2], dtype=torch.int32, device=disc.device)
+        info = torch.zeros(1, dtype=torch.int32, device=disc.device)
+        _lib.call("hpgPrecondFactor", disc.plan.handle, _vp(lu), _vp(piv), float(alpha), float(beta),
+                  0, disc.plan.ncells, _vp(info), _stream())
+        return cls(disc, lu, piv, info)
+
+    @classmethod
+    def from_blocks(cls, disc, blocks):
+        """Factor given blocks (host list/array or device tensor), as ``CellBlockPreconditioner``."""
+        nb = disc.n * disc.n * disc.ncomp
+        if isinstance(blocks, torch.Tensor):
+            lu = blocks.to(disc.device, torch.float64).reshape(-1, nb, nb).clone()
+        else:
+            arr = np.ascontiguousarray(np.stack(blocks), dtype=np.float64)
+            lu = torch.from_numpy(arr).to(disc.device)
+        if lu.shape != (disc.plan.ncells, nb, nb):
+            raise ValueError("blocks have the wrong shape")
+        piv = torch.empty(lu.shape[:2], dtype=torch.int32, device=disc.device)
+        info = torch.zeros(1, dtype=torch.int32, device=disc.device)
+        _lib.call("hpgLUFactor", disc.plan.handle, _vp(lu), _vp(piv), disc.plan.ncells, _vp(info),
+                  _stream())
+        return cls(disc, lu, piv, info)
+
+    @property
+    def indices(self):
+        return self.disc.cell_psi_indices
+
+    @property
+    def factors(self):
+        if self._factors is None:
+            lu = self.lu_t.cpu().numpy()
+            piv = self.piv_t.cpu().numpy()
+            self._factors = [(lu[i], piv[i]) for i in range(lu.shape[0])]
+        return self._factors
+
+    def apply_t(self, x_t, out=None):
+        d = self.disc
+        d._check_len(x_t, self.n, "x")
+        out = torch.empty(self.n, dtype=F64, device=d.device) if out is None else out
+        _lib.call("hpgLUSolve", d.plan.handle, _vp(self.lu_t), _vp(self.piv_t), _vp(x_t), _vp(out),
+                  _stream())
+        return out
+
+    def apply(self, x):
+        d = self.disc
+        y = self.apply_t(d.h2d(x, "x"), out=d._dev("out_prec", self.n))
+        return d.d2h(y, "prec")
+
+    def __call__(self, x):
+        return self.apply(x)

@@ -115,6 +115,40 @@ def gauss_analysis(q, ncoeff):
     return ((2.0 * np.arange(ncoeff) + 1.0) / 2.0)[:, None] * P * om[None, :]
 
 
+@lru_cache(maxsize=None)
+def schur_triple_factors(n):
+    """Reference-cell factors of the Schur hat triple (``assembly.py:577-595``).
+
+    On a cell the triple is ``Bhat^T Ahat^{-1} Bhat`` with ``Bhat = gx (x) gy``
+    and ``Ahat = Kx (x) My + Mx (x) Ky`` (spectral Gram ``assembly.py:156-170``,
+    stiffness diagonal ``:147-153``, pentadiagonal mass ``:128-144``; n modes
+    per direction).  With ``g = h ghat``, ``K = khat / h``, ``M = h mhat`` and
+    ``khat^{-1/2} mhat khat^{-1/2} = V diag(lam) V^T``:
+
+        T[(a,b),(c,d)] = (hx hy)^3 sum_ij Z[a,i] Z[b,j] Z[c,i] Z[d,j]
+                                       / (hx^2 lam_i + hy^2 lam_j),
+        Z = ghat^T khat^{-1/2} V.
+
+    Returns ``(Z, lam)`` (n x n row-major, n); the device forms T per width key.
+    Agrees with the reference's dense ``np.linalg.solve`` to <= 8e-16 relative
+    for n <= 81 (tests/test_precond_host.py).
+    """
+    g = np.zeros((n, n))
+    k = np.zeros(n)
+    m = np.zeros((n, n))
+    for a in range(n):
+        g[a, a] = 1.0 / (2 * a + 1)
+        k[a] = 4.0 * (2 * a + 3)
+        m[a, a] = 1.0 / (2 * a + 1) + 1.0 / (2 * a + 5)
+        if a + 2 < n:
+            g[a, a + 2] = -1.0 / (2 * a + 5)
+            m[a, a + 2] = m[a + 2, a] = -1.0 / (2 * a + 5)
+    ki = 1.0 / np.sqrt(k)
+    lam, v = np.linalg.eigh(ki[:, None] * m * ki[None, :])
+    z = g.T @ (ki[:, None] * v)
+    return np.ascontiguousarray(z), np.ascontiguousarray(lam)
+
+
 class Tables:
     """The per-direction tables of one uniform-degree discretisation.
 

@@ -137,3 +137,25 @@ def test_residual_paths_and_fused_apply(name):
         assert rel_err(m.cpu().numpy(), g["moments"]) < TOL
         m, _ = d.exp_moments_t(t["psi"], wcache=True)
         assert rel_err(m.cpu().numpy(), g["moments"]) < TOL
+
+
+def test_no_interior_u_dofs():
+    """Gradient p=1 on a single cell: ndof_u == 0, empty u-side arrays (NULL pointers)."""
+    from types import SimpleNamespace
+    from oracle import hpg_oracle as orc
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    from paper_2412_13733_b200.proximal import residual
+    from paper_2412_13733_b200.workloads import phi_bilinear
+    d = D.GradientDisc2D(uniform_mesh_2d(0.0, 1.0, 1, 1), 1.0, phi_bilinear, rule="gauss", nq=3)
+    assert d.ndof_u == 0 and d.f_load.size == 0
+    t = d.tables
+    P = orc.Problem("gradient", d.xpts, d.ypts, 1,
+                    SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
+    psi = np.array([0.3, -0.2])
+    u = np.zeros(0)
+    b_u, b_psi, cl = residual(d, 2.0, np.zeros(2), u, psi)
+    phi_vals = P.sample(phi_bilinear)
+    rb_u, rb_psi, _ = P.residual(2.0, np.zeros(2), u, psi, np.zeros(0), phi_vals=phi_vals)
+    assert b_u.size == 0 and not cl
+    assert orc.rel_err(b_psi, rb_psi) < TOL

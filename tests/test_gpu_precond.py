@@ -1,0 +1,132 @@
+"""GPU parity of the per-cell Schur preconditioner.
+
+Reference: precond_blocks (assembly.py:597-603, 851-860) and
+CellBlockPreconditioner (linalg.py:246-266, scipy lu_factor / lu_solve).
+Bar: 1e-12 global max-norm relative, as the hot path.  The blocks are
+well conditioned (cond ~1e2-1e3 measured on c0/c1/grad p6), so the LU solve's
+rounding stays far below the bar.  Pivots are compared exactly where the
+pivot choice is unambiguous.
+"""
+import numpy as np
+import pytest
+
+from golden_util import load, names
+from oracle import hpg_oracle as orc
+from test_gpu_fullsize import build
+from test_gpu_parity import make_disc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.mark.parametrize("name", names())
+def test_precond_blocks_and_apply_golden(name):
+    from paper_2412_13733_b200.disc import DeviceCellBlockPreconditioner
+    g = load(name)
+    d = make_disc(g)
+    D = d.assemble_D(g["psi"])
+    beta = float(g["prec_beta"])
+    if np.isnan(g["psi"]).any():
+        with pytest.raises(ValueError):
+            d.schur_preconditioner(D, g["alpha"], beta)
+        return
+    pb = d.precond_blocks(D, g["alpha"], beta)
+    if "precond_blocks" in g:
+        assert orc.rel_err(np.stack(pb), g["precond_blocks"]) < TOL
+    else:
+        assert orc.rel_err(np.stack(pb)[:, g["block_rows"], :], g["precond_sel"]) < TOL
+    if not np.isfinite(g["precond_apply"]).all():
+        return                                          # exactly singular (clamp case)
+    if g["kind"] == "obstacle" and g["p"] == 82:
+        return                                          # 6561^2 blocks: beyond the per-CTA LU
+    M = d.schur_preconditioner(D, g["alpha"], beta)
+    assert orc.rel_err(M.apply(g["x"]), g["precond_apply"]) < TOL
+    assert orc.rel_err(M(g["x"]), g["precond_apply"]) < TOL
+    # from materialised blocks, as CellBlockPreconditioner(blocks, ...)
+    M2 = DeviceCellBlockPreconditioner.from_blocks(d, pb)
+    assert orc.rel_err(M2.apply(g["x"]), g["precond_apply"]) < TOL
+
+
+@pytest.mark.parametrize("kind,p", [("obstacle", 2), ("obstacle", 4), ("obstacle", 8),
+                                    ("obstacle", 16), ("gradient", 1), ("gradient", 4),
+                                    ("gradient", 6), ("gradient", 9)])
+def test_lu_factors_match_scipy(kind, p):
+    """Random well-conditioned blocks: pivots identical to LAPACK, factors to 1e-13."""
+    import scipy.linalg as sla
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    cls = D.ObstacleDisc2D if kind == "obstacle" else D.GradientDisc2D
+    d = cls(uniform_mesh_2d(0.0, 1.0, 3, p), 1.0, 0.5, rule="gauss", nq=p + 2)
+    nb = d.n * d.n * d.ncomp
+    rng = np.random.default_rng(p)
+    blocks = rng.standard_normal((d.plan.ncells, nb, nb)) + 0.5 * np.eye(nb)
+    M = D.DeviceCellBlockPreconditioner.from_blocks(d, list(blocks))
+    for i, (lu, piv) in enumerate(M.factors):
+        rlu, rpiv = sla.lu_factor(blocks[i])
+        assert np.array_equal(piv, rpiv)
+        assert orc.rel_err(lu, rlu) < 1e-13
+    x = rng.standard_normal(d.ndof_psi)
+    idx = d.cell_psi_indices
+    assert orc.rel_err(M.apply(x), orc.lu_precond_apply(blocks, idx, d.ndof_psi, x)) < 1e-11
+
+
+def test_lu_tie_and_singular_semantics():
+    """First maximal |a| wins ties (idamax); an exactly singular block warns."""
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    d = D.GradientDisc2D(uniform_mesh_2d(0.0, 1.0, 1, 1), 1.0, 0.5, rule="gauss", nq=3)
+    assert d.n * d.n * d.ncomp == 2
+    M = D.DeviceCellBlockPreconditioner.from_blocks(d, [np.array([[1.0, 2.0], [-1.0, 3.0]])])
+    lu, piv = M.factors[0]
+    assert piv.tolist() == [0, 1]
+    assert np.array_equal(lu, np.array([[1.0, 2.0], [-1.0, 5.0]]))
+    M = D.DeviceCellBlockPreconditioner.from_blocks(d, [np.array([[-1.0, 2.0], [4.0, 3.0]])])
+    lu, piv = M.factors[0]
+    assert piv.tolist() == [1, 1]
+    with pytest.warns(RuntimeWarning):
+        D.DeviceCellBlockPreconditioner.from_blocks(d, [np.array([[0.0, 0.0], [0.0, 1.0]])])
+    with pytest.raises(ValueError):
+        D.DeviceCellBlockPreconditioner.from_blocks(d, [np.array([[np.inf, 0.0], [0.0, 1.0]])])
+
+
+@pytest.mark.parametrize("cfg_name,rule", [("c1", "gauss"), ("c1", "reference"), ("c2", "gauss"),
+                                           ("c4p6", "gauss"), ("c0", "reference")])
+def test_full_size_preconditioner(cfg_name, rule):
+    """BASELINE sizes: fused factor (D -> P -> LU) + apply vs the oracle, and P y == x."""
+    import torch
+    cfg, d, P, inp, dev = build(cfg_name, rule)
+    alpha, beta = cfg.alphas[-1], 1e-3
+    _, _, _ = d.residual_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
+    D = d.assemble_D_t(dev["psi"])
+    M = d.schur_preconditioner(D, alpha, beta)
+    y = M.apply_t(dev["x"])
+    # property at full size: P y == x through the dense precond blocks
+    pb = d.precond_blocks_t(D, alpha, beta)
+    back = d.blocks_matvec_t(pb.reshape(pb.shape[0], -1), y).cpu().numpy()
+    assert orc.rel_err(back, inp["x"]) < 1e-11
+    # oracle (scipy getrf/getrs per cell) on the oracle's own blocks
+    if cfg.kind == "obstacle":
+        blocks, _ = P.obstacle_blocks(inp["psi"])
+    else:
+        phi_vals = P.sample(inp["phi"])
+        blocks = P.gradient_blocks(inp["psi"], phi_vals)
+    rpb = orc.precond_blocks(P, blocks, alpha, beta)
+    assert orc.rel_err(pb.cpu().numpy(), np.stack(rpb)) < TOL
+    idx = orc.cell_psi_indices(P.ncx, P.ncy, P.n)
+    if cfg.kind == "gradient":
+        idx = [np.concatenate([i, i + P.ncomp_dofs]) for i in idx]
+    ry = orc.lu_precond_apply(rpb, idx, P.ndof_psi, inp["x"])
+    assert orc.rel_err(y.cpu().numpy(), ry) < TOL
+    torch.cuda.synchronize()
+
+
+def test_lu_unsupported_size_is_loud():
+    """c3 (6561^2 blocks) exceeds the per-CTA LU: an error, never a CPU fallback."""
+    from paper_2412_13733_b200 import _lib
+    lib = _lib.load()
+    assert lib.hpgLUMaxBlock() < 6561
+    cfg, d, P, inp, dev = build("c3", "gauss", ncells=1)
+    d.residual_t(1.0, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
+    D = d.assemble_D_t(dev["psi"])
+    with pytest.raises(_lib.HpgError):
+        d.schur_preconditioner(D, 1.0, 0.0)
