@@ -132,21 +132,33 @@ int hpgLoadVector(hpgPlan plan, const double* vals, double* out, void* stream);
  * (device int, may be NULL) is OR-ed with 1 if an entry is non-finite (scipy's
  * check_finite raises ValueError there) and 2 on an exactly zero pivot
  * (LAPACK info > 0; scipy warns).
+ * `perm` (nullable, [count][nb]) also receives the composed interchanges
+ * (position i <- row perm[i]), which lets the solve gather instead of
+ * replaying the swaps.
  * hpgPrecondFactor: both, fused (blocks hold D on entry, LU of P on exit).
  * hpgLUSolve: CellBlockPreconditioner.apply (linalg.py:253-257):
- * y[idx_e] = lu_solve(LU_e, x[idx_e]) for every cell.
+ * y[idx_e] = lu_solve(LU_e, x[idx_e]) for every cell (perm nullable).
  * hpgLUMaxBlock: largest block side the per-CTA factorisation supports. */
 int hpgPrecondPrepare(hpgPlan plan, const double* Zhat, const double* lam_hat,
                       void* stream);
 int hpgPrecondBlocks(hpgPlan plan, double* blocks, double alpha, double beta,
                      int c0, int count, void* stream);
-int hpgLUFactor(hpgPlan plan, double* blocks, int* ipiv, int count,
+/* precond_blocks straight from the cached point weights of D (the blocks
+ * kernel's epilogue writes P_e instead of D_e; same layout as hpgBlocks). */
+int hpgPrecondAssemble(hpgPlan plan, const double* wcache, double alpha,
+                       double beta, double* blocks, int c0, int count,
+                       void* stream);
+int hpgLUFactor(hpgPlan plan, double* blocks, int* ipiv, int* perm, int count,
                 int* info, void* stream);
-int hpgPrecondFactor(hpgPlan plan, double* blocks, int* ipiv, double alpha,
-                     double beta, int c0, int count, int* info, void* stream);
+int hpgPrecondFactor(hpgPlan plan, double* blocks, int* ipiv, int* perm,
+                     double alpha, double beta, int c0, int count, int* info,
+                     void* stream);
 int hpgLUSolve(hpgPlan plan, const double* lu, const int* ipiv,
-               const double* x, double* y, void* stream);
+               const int* perm, const double* x, double* y, void* stream);
 int hpgLUMaxBlock(void);
+/* Tuning aid: device array of 8 cycle counters the CTA LU accumulates per
+ * phase into (NULL disables; off by default). */
+int hpgLUProfile(unsigned long long* counters);
 
 const char* hpgLastError(void);
 int hpgVersion(void);

@@ -39,10 +39,12 @@ SIGNATURES = {
     "hpgLoadVector": [_P, _P, _P, _P],
     "hpgPrecondPrepare": [_P, _P, _P, _P],
     "hpgPrecondBlocks": [_P, _P, _D, _D, _I, _I, _P],
-    "hpgLUFactor": [_P, _P, _P, _I, _P, _P],
-    "hpgPrecondFactor": [_P, _P, _P, _D, _D, _I, _I, _P, _P],
-    "hpgLUSolve": [_P, _P, _P, _P, _P, _P],
+    "hpgPrecondAssemble": [_P, _P, _D, _D, _P, _I, _I, _P],
+    "hpgLUFactor": [_P, _P, _P, _P, _I, _P, _P],
+    "hpgPrecondFactor": [_P, _P, _P, _P, _D, _D, _I, _I, _P, _P],
+    "hpgLUSolve": [_P, _P, _P, _P, _P, _P, _P],
     "hpgLUMaxBlock": [],
+    "hpgLUProfile": [_P],
     "hpgVersion": [],
 }
 

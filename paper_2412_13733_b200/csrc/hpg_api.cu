@@ -477,14 +477,18 @@ static int blocks_gemm(hpgPlan P, const double* wcache, double* blocks, int c0, 
   return HPG_OK;
 }
 
-int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {
+static int blocks_impl(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream,
+                       int prec, double alpha, double beta) {
   if (int rc = check(P)) return rc;
   if (!wcache || !blocks) return fail(HPG_ERR_ARG, "null pointer");
   if (c0 < 0 || count < 0 || c0 + count > P->N) return fail(HPG_ERR_ARG, "cell range out of bounds");
+  if (prec && P->kind == HPG_OBSTACLE && P->nkeys == 0)
+    return fail(HPG_ERR_ARG, "hpgPrecondPrepare has not been called on this plan");
   if (count == 0) return HPG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   BArgs B;
   memset(&B, 0, sizeof(B));
+  B.prec = prec; B.alpha = alpha; B.beta = beta; B.tri = P->tri; B.key = P->cell_key;
   B.n = P->n; B.NT = P->NT; B.QT = P->QT; B.nq = P->nq;
   B.nf = P->kind == HPG_OBSTACLE ? 1 : 3;
   B.ncy = P->ncy; B.cell0 = c0; B.ncell = count;
@@ -505,7 +509,16 @@ int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count
   }
   if (smem > ((size_t)200 << 10) || P->NT > 4) {
     // large tiles: two-stage GEMM (Z = G W, blocks = Z G^T) through global scratch
-    return blocks_gemm(P, wcache, blocks, c0, count, s);
+    int rc = blocks_gemm(P, wcache, blocks, c0, count, s);
+    if (rc || !prec) return rc;
+    PrecArgs A;
+    memset(&A, 0, sizeof(A));
+    A.kind = P->kind; A.n = P->n; A.n2 = P->n * P->n;
+    A.nb = A.n2 * (P->kind == HPG_OBSTACLE ? 1 : 2);
+    A.ncy = P->ncy; A.cell0 = c0; A.count = count; A.transform = 1;
+    A.alpha = alpha; A.beta = beta; A.hx = P->hx; A.hy = P->hy; A.tri = P->tri; A.key = P->cell_key;
+    A.M = blocks;
+    return launch_precond_transform(A, s);
   }
   void* fn;
   switch (P->NT) {
@@ -535,6 +548,15 @@ int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count
   void* args[] = {&B};
   CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, s));
   return HPG_OK;
+}
+
+int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {
+  return blocks_impl(P, wcache, blocks, c0, count, stream, 0, 1.0, 0.0);
+}
+
+int hpgPrecondAssemble(hpgPlan P, const double* wcache, double alpha, double beta, double* blocks, int c0,
+                       int count, void* stream) {
+  return blocks_impl(P, wcache, blocks, c0, count, stream, 1, alpha, beta);
 }
 
 int hpgBlocksMatvec(hpgPlan P, const double* blocks, const double* x, double* y, void* stream) {
@@ -654,8 +676,11 @@ int hpgPrecondPrepare(hpgPlan P, const double* Zhat, const double* lam_hat, void
   return HPG_OK;
 }
 
-static int prec_args(hpgPlan P, double* blocks, int* ipiv, int* info, double alpha, double beta, int c0,
-                     int count, int transform, PrecArgs* A) {
+// tools only: per-phase cycle counters of the CTA LU (hpgLUProfile)
+static unsigned long long* g_lu_prof = nullptr;
+
+static int prec_args(hpgPlan P, double* blocks, int* ipiv, int* perm, int* info, double alpha, double beta,
+                     int c0, int count, int transform, PrecArgs* A) {
   if (!blocks) return fail(HPG_ERR_ARG, "null pointer");
   if (c0 < 0 || count < 0 || c0 + count > P->N) return fail(HPG_ERR_ARG, "cell range out of bounds");
   if (transform && P->kind == HPG_OBSTACLE && P->nkeys == 0)
@@ -666,45 +691,52 @@ static int prec_args(hpgPlan P, double* blocks, int* ipiv, int* info, double alp
   A->ncy = P->ncy; A->cell0 = c0; A->count = count; A->transform = transform;
   A->alpha = alpha; A->beta = beta;
   A->hx = P->hx; A->hy = P->hy; A->tri = P->tri; A->key = P->cell_key;
-  A->M = blocks; A->ipiv = ipiv; A->info = info;
+  A->M = blocks; A->ipiv = ipiv; A->info = info; A->perm = perm;
+  A->prof = g_lu_prof;
   return HPG_OK;
 }
 
 int hpgPrecondBlocks(hpgPlan P, double* blocks, double alpha, double beta, int c0, int count, void* stream) {
   if (int rc = check(P)) return rc;
   PrecArgs A;
-  if (int rc = prec_args(P, blocks, nullptr, nullptr, alpha, beta, c0, count, 1, &A)) return rc;
+  if (int rc = prec_args(P, blocks, nullptr, nullptr, nullptr, alpha, beta, c0, count, 1, &A)) return rc;
   if (count == 0) return HPG_OK;
   return launch_precond_transform(A, (cudaStream_t)stream);
 }
 
-int hpgLUFactor(hpgPlan P, double* blocks, int* ipiv, int count, int* info, void* stream) {
+int hpgLUFactor(hpgPlan P, double* blocks, int* ipiv, int* perm, int count, int* info, void* stream) {
   if (int rc = check(P)) return rc;
   PrecArgs A;
-  if (int rc = prec_args(P, blocks, ipiv, info, 1.0, 0.0, 0, count, 0, &A)) return rc;
+  if (int rc = prec_args(P, blocks, ipiv, perm, info, 1.0, 0.0, 0, count, 0, &A)) return rc;
   if (!ipiv) return fail(HPG_ERR_ARG, "null pivot array");
   if (count == 0) return HPG_OK;
   return launch_lu(A, P->nsm, (cudaStream_t)stream);
 }
 
-int hpgPrecondFactor(hpgPlan P, double* blocks, int* ipiv, double alpha, double beta, int c0, int count,
-                     int* info, void* stream) {
+int hpgPrecondFactor(hpgPlan P, double* blocks, int* ipiv, int* perm, double alpha, double beta, int c0,
+                     int count, int* info, void* stream) {
   if (int rc = check(P)) return rc;
   PrecArgs A;
-  if (int rc = prec_args(P, blocks, ipiv, info, alpha, beta, c0, count, 1, &A)) return rc;
+  if (int rc = prec_args(P, blocks, ipiv, perm, info, alpha, beta, c0, count, 1, &A)) return rc;
   if (!ipiv) return fail(HPG_ERR_ARG, "null pivot array");
   if (count == 0) return HPG_OK;
   return launch_lu(A, P->nsm, (cudaStream_t)stream);
 }
 
-int hpgLUSolve(hpgPlan P, const double* lu, const int* ipiv, const double* x, double* y, void* stream) {
+int hpgLUSolve(hpgPlan P, const double* lu, const int* ipiv, const int* perm, const double* x, double* y,
+               void* stream) {
   if (int rc = check(P)) return rc;
   if (!lu || !ipiv || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs E = base_args(P);
   const int nb = P->n * P->n * (P->kind == HPG_OBSTACLE ? 1 : 2);
-  return launch_lu_solve(E, lu, ipiv, nb, x, y, (cudaStream_t)stream);
+  return launch_lu_solve(E, lu, ipiv, perm, nb, x, y, (cudaStream_t)stream);
 }
 
 int hpgLUMaxBlock(void) { return lu_max_nb(); }
+
+int hpgLUProfile(unsigned long long* counters) {
+  g_lu_prof = counters;
+  return HPG_OK;
+}
 
 }  // extern "C"

@@ -14,6 +14,7 @@
 #pragma once
 #include "hpg_common.cuh"
 #include "hpg_elem.cuh"
+#include "hpg_precond.cuh"
 
 namespace hpg {
 
@@ -29,6 +30,11 @@ struct BArgs {
   long long nb;            // block side (n^2 or 2 n^2)
   const double* hx;
   const double* hy;
+  // optional fused epilogue: write P_e = -(D_e + E_beta + T/alpha) instead of D_e
+  int prec;
+  double alpha, beta;
+  const double* tri;       // obstacle triples [nkeys][n2][n2]
+  const int* key;          // [N] cell -> triple key
 };
 
 constexpr int BR_MAXACC = 24;   // 8x8 accumulator tiles per warp
@@ -144,12 +150,19 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
         k += dk;
         if (k >= n) { k -= n; ++j; }
         if (B.nf == 1 || f == 0) {
-          blk[row * B.nb + idx] = v;
+          blk[row * B.nb + idx] = B.prec ? precond_entry(B.nf == 1 ? 0 : 1, n, (int)n2, B.hx[cx], B.hy[cy], B.alpha,
+                                                         B.beta, B.nf == 1 ? B.tri + (size_t)B.key[e] * n2 * n2 : nullptr,
+                                                         (int)row, idx, v)
+                                         : v;
         } else if (f == 1) {
-          blk[row * B.nb + n2 + idx] = v;
-          blk[(n2 + row) * B.nb + idx] = v;
+          const double w = B.prec ? -v : v;
+          blk[row * B.nb + n2 + idx] = w;
+          blk[(n2 + row) * B.nb + idx] = w;
         } else {
-          blk[(n2 + row) * B.nb + n2 + idx] = v;
+          blk[(n2 + row) * B.nb + n2 + idx] =
+              B.prec ? precond_entry(1, n, (int)n2, B.hx[cx], B.hy[cy], B.alpha, B.beta, nullptr, (int)(n2 + row),
+                                     (int)(n2 + idx), v)
+                     : v;
         }
       }
       if (B.per_warp) __syncwarp(); else __syncthreads();

@@ -66,39 +66,11 @@ __global__ void k_triple(const double* __restrict__ Z, const double* __restrict_
   }
 }
 
-// spectral mass entry (assembly.py:128-144) and stiffness diagonal (:147-153)
-__device__ __forceinline__ double smass(int a, int c, double h) {
-  if (a == c) return h * (1.0 / (2 * a + 1) + 1.0 / (2 * a + 5));
-  if (a - c == 2 || c - a == 2) return -h / (2 * (a < c ? a : c) + 5);
-  return 0.0;
-}
-__device__ __forceinline__ double sstiff(int a, double h) { return 4.0 * (2.0 * a + 3.0) / h; }
-
 // P_e[row][col] from D_e[row][col] = v
 __device__ __forceinline__ double precond_value(const PrecArgs& A, int e, int row, int col, double v) {
   const int cx = e / A.ncy, cy = e - (e / A.ncy) * A.ncy;
-  const double hx = A.hx[cx], hy = A.hy[cy];
-  if (A.kind == HPG_OBSTACLE) {
-    double t = -v - A.tri[((size_t)A.key[e] * A.n2 + row) * A.n2 + col] / A.alpha;
-    if (row == col) {
-      const int a = row / A.n, b = row - (row / A.n) * A.n;
-      t -= A.beta * ((hx / (2.0 * a + 1.0)) * (hy / (2.0 * b + 1.0)));
-    }
-    return t;
-  }
-  double t = -v;
-  if (A.beta != 0.0) {
-    const int cr = row / A.n2, cc = col / A.n2;
-    if (cr == cc) {
-      const int rr = row - cr * A.n2, c2 = col - cc * A.n2;
-      const int a = rr / A.n, b = rr - (rr / A.n) * A.n;
-      const int c = c2 / A.n, d = c2 - (c2 / A.n) * A.n;
-      const double e1 = (a == c) ? sstiff(a, hx) * smass(b, d, hy) : 0.0;
-      const double e2 = (b == d) ? smass(a, c, hx) * sstiff(b, hy) : 0.0;
-      t -= A.beta * (e1 + e2);
-    }
-  }
-  return t;
+  const double* tri = A.kind == HPG_OBSTACLE ? A.tri + (size_t)A.key[e] * A.n2 * A.n2 : nullptr;
+  return precond_entry(A.kind, A.n, A.n2, A.hx[cx], A.hy[cy], A.alpha, A.beta, tri, row, col, v);
 }
 
 __global__ void k_precond_transform(PrecArgs A) {
@@ -123,7 +95,7 @@ __device__ __forceinline__ void argmax_combine(double& best, int& bi, double ov,
 }
 
 template <int KB>
-__global__ void __launch_bounds__(LU_THREADS) k_lu(PrecArgs A) {
+__global__ void __launch_bounds__(LU_THREADS, 2) k_lu(PrecArgs A) {
   extern __shared__ double sm[];
   constexpr int LDP = KB + 1;
   constexpr int NOPIV = 0x7fffffff;
@@ -135,24 +107,44 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu(PrecArgs A) {
   double* sRv = sU + KB * LU_ULD;                   // per-warp argmax values [8]
   int* sRi = reinterpret_cast<int*>(sRv + 8);       // and rows [8]
   int* sPiv = sRi + 8;                              // panel pivots [KB]
+  int* sList = sPiv + KB;                           // rows touched by the interchanges [2 KB + 1]
+  int* sRow = sList + 2 * KB + 1;                   // composed interchanges: position <- row [nb]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, c = lane & 3;
+  // phase profiling (A.prof != nullptr only from tools/prof_precond.py):
+  // cycles since the previous mark are charged to the phase that just ended
+  long long t_last = clock64();
+  int ph_last = 7;
+#define PROF_MARK(ph)                                                   \
+  do {                                                                  \
+    if (A.prof != nullptr && tid == 0) {                                \
+      const long long t_now = clock64();                                \
+      atomicAdd(A.prof + ph_last, (unsigned long long)(t_now - t_last)); \
+      t_last = t_now;                                                   \
+    }                                                                   \
+    ph_last = (ph);                                                     \
+  } while (0)
 
   for (int cl = blockIdx.x; cl < A.count; cl += gridDim.x) {
     double* M = A.M + (size_t)cl * nb * nb;
     int* piv = A.ipiv + (size_t)cl * nb;
+    PROF_MARK(6);
     if (A.transform) {
       const int e = A.cell0 + cl;
-      for (long long idx = tid; idx < (long long)nb * nb; idx += LU_THREADS) {
-        const int row = (int)(idx / nb), col = (int)(idx - (long long)row * nb);
+#pragma unroll 4
+      for (int idx = tid; idx < nb * nb; idx += LU_THREADS) {
+        const int row = idx / nb, col = idx - (idx / nb) * nb;
         M[idx] = precond_value(A, e, row, col, M[idx]);
       }
       __syncthreads();
     }
     for (int k0 = 0; k0 < nb; k0 += KB) {
       const int kb = nb - k0 < KB ? nb - k0 : KB, rows = nb - k0;
+      PROF_MARK(0);
       // (1) load the panel; each thread tracks its rows' max |a| of column 0
       bool bad = false;
+      for (int i = tid; i < rows; i += LU_THREADS) sRow[i] = i;
+#pragma unroll 4
       for (int idx = tid; idx < rows * KB; idx += LU_THREADS) {
         const int i = idx / KB, j = idx - (idx / KB) * KB;
         const double v = j < kb ? M[(size_t)(k0 + i) * nb + k0 + j] : 0.0;
@@ -164,6 +156,7 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu(PrecArgs A) {
       }
       if (bad && A.info) atomicOr(A.info, 1);
       __syncthreads();
+      PROF_MARK(7);
       double best = -1.0;
       int bi = NOPIV;
       for (int i = tid; i < rows; i += LU_THREADS) {
@@ -215,43 +208,85 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu(PrecArgs A) {
         // warp reduction; the barrier after its smem write orders this update
         __syncthreads();
       }
+      PROF_MARK(1);
       // (4) panel back to global; interchanges applied to the other columns
+#pragma unroll 4
       for (int idx = tid; idx < rows * kb; idx += LU_THREADS) {
         const int i = idx / kb, j = idx - (idx / kb) * kb;
         M[(size_t)(k0 + i) * nb + k0 + j] = sP[i * LDP + j];
       }
-      for (int col = tid; col < nb; col += LU_THREADS) {
-        if (col >= k0 && col < k0 + kb) continue;
+      // the panel's interchanges, composed: position q receives row sRow[q];
+      // touched positions = 0..kb-1 plus the distinct pivot rows >= kb
+      if (tid == 0) {
         for (int j = 0; j < kb; ++j) {
           const int p = sPiv[j];
           if (p != j) {
-            const double t = M[(size_t)(k0 + j) * nb + col];
-            M[(size_t)(k0 + j) * nb + col] = M[(size_t)(k0 + p) * nb + col];
-            M[(size_t)(k0 + p) * nb + col] = t;
+            const int t = sRow[j];
+            sRow[j] = sRow[p];
+            sRow[p] = t;
           }
         }
       }
+      if (warp == 1) {
+        const int q = lane < kb ? sPiv[lane] : -1;
+        const bool extra = q >= kb;
+        const unsigned grp = __match_any_sync(~0u, extra ? q : -1 - lane);
+        const bool lead = extra && (__ffs(grp) - 1 == lane);
+        const unsigned bal = __ballot_sync(~0u, lead);
+        if (lead) sList[kb + __popc(bal & ((1u << lane) - 1))] = q;
+        if (lane < kb) sList[lane] = lane;
+        if (lane == 0) sList[2 * KB] = kb + __popc(bal);
+      }
       __syncthreads();
+      {
+      PROF_MARK(2);
+        // apply them to the columns outside the panel, 64 columns at a time:
+        // gather the touched rows into shared memory (sA..sU, free here),
+        // then scatter them to their positions -- independent coalesced loads
+        const int cnt = sList[2 * KB];
+        double* sG = sA;                                  // [2 KB][64]
+        for (int cb = 0; cb < nb; cb += 64) {
+#pragma unroll 4
+          for (int idx = tid; idx < cnt * 64; idx += LU_THREADS) {
+            const int t = idx >> 6, col = cb + (idx & 63);
+            if (col < nb && (col < k0 || col >= k0 + kb))
+              sG[idx] = M[(size_t)(k0 + sRow[sList[t]]) * nb + col];
+          }
+          __syncthreads();
+#pragma unroll 4
+          for (int idx = tid; idx < cnt * 64; idx += LU_THREADS) {
+            const int t = idx >> 6, col = cb + (idx & 63);
+            if (col < nb && (col < k0 || col >= k0 + kb))
+              M[(size_t)(k0 + sList[t]) * nb + col] = sG[idx];
+          }
+          __syncthreads();
+        }
+      }
+      PROF_MARK(3);
       // (5) Linv = L11^{-1} (unit lower), one column per thread; zero outside
       //     the kb x kb corner so padded k-steps below contribute exact zeros
       if (tid < KB) {
+        // column cc of L11^{-1}: t = e_cc, then t_i -= L_ij t_j for j < i in
+        // axpy order -- straight-line, every t_j final before it is used
         const int cc = tid;
-        for (int i = 0; i < KB; ++i) {
-          double t = 0.0;
-          if (i == cc) {
-            t = 1.0;
-          } else if (i > cc) {
-            for (int j = cc; j < i; ++j) t -= sP[i * LDP + j] * sLi[j * LDP + cc];
-          }
-          sLi[i * LDP + cc] = (i < kb && cc < kb) ? t : 0.0;
-        }
+        double t[KB];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) t[i] = i == cc ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < KB - 1; ++j)
+#pragma unroll
+          for (int i = j + 1; i < KB; ++i) t[i] -= sP[i * LDP + j] * t[j];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) sLi[i * LDP + cc] = (i < kb && cc < kb) ? t[i] : 0.0;
       }
       __syncthreads();
+      PROF_MARK(4);
       // (6) per 64-column chunk: U12 = Linv A12 and A22 -= L21 U12, both on
       //     the FP64 tensor cores with the chunk staged in shared memory
       const int trows = rows - kb;
       const int nrt = (trows + 7) >> 3;
       for (int cc0 = k0 + kb; cc0 < nb; cc0 += LU_UCH) {
+#pragma unroll 4
         for (int idx = tid; idx < KB * LU_UCH; idx += LU_THREADS) {
           const int j = idx / LU_UCH, t = idx - (idx / LU_UCH) * LU_UCH;
           const int col = cc0 + t;
@@ -297,95 +332,132 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu(PrecArgs A) {
         }
         __syncthreads();
       }
+      PROF_MARK(5);
+    }
+    if (A.perm != nullptr) {
+      // composed interchanges: solve-side gather x'[i] = x[perm[i]] (getrs' laswp)
+      for (int i = tid; i < nb; i += LU_THREADS) sRow[i] = i;
+      __syncthreads();
+      if (tid == 0) {
+        for (int i = 0; i < nb; ++i) {
+          const int p = piv[i];
+          if (p != i) {
+            const int t = sRow[i];
+            sRow[i] = sRow[p];
+            sRow[p] = t;
+          }
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < nb; i += LU_THREADS) A.perm[(size_t)cl * nb + i] = sRow[i];
     }
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(SOLVE_THREADS) k_lu_solve(ElemArgs E, const double* __restrict__ lu,
-                                                            const int* __restrict__ ipiv, int nb,
+__global__ void __launch_bounds__(SOLVE_THREADS, 8) k_lu_solve(ElemArgs E, const double* __restrict__ lu,
+                                                            const int* __restrict__ ipiv,
+                                                            const int* __restrict__ perm, int nb,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ y) {
   extern __shared__ double sx[];
-  int* sp = reinterpret_cast<int*>(sx + nb);
+  double* sD = sx + nb;                              // diagonal block [32][33]
+  int* sp = reinterpret_cast<int*>(sD + 32 * 33);
   const int e = blockIdx.x;
   const int cx = e / E.ncy, cy = e - cx * E.ncy;
   const int n2 = E.n * E.n;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int NW = SOLVE_THREADS / 32;
   const double* L = lu + (size_t)e * nb * nb;
-  for (int l = tid; l < nb; l += SOLVE_THREADS) {
-    const int comp = l / n2, rem = l - comp * n2;
-    sx[l] = __ldg(x + comp * E.ncomp + psi_index(E, cx, cy, rem / E.n, rem % E.n));
-    sp[l] = __ldg(ipiv + (size_t)e * nb + l);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int i = 0; i < nb; ++i) {
-      const int p = sp[i];
-      if (p != i) {
-        const double t = sx[i];
-        sx[i] = sx[p];
-        sx[p] = t;
+  // (1) x restricted to the cell, rows interchanged (getrs' laswp)
+  if (perm != nullptr) {
+    for (int l = tid; l < nb; l += SOLVE_THREADS) {
+      const int q = __ldg(perm + (size_t)e * nb + l);
+      const int comp = q / n2, rem = q - comp * n2;
+      sx[l] = __ldg(x + comp * E.ncomp + psi_index(E, cx, cy, rem / E.n, rem % E.n));
+    }
+  } else {
+    for (int l = tid; l < nb; l += SOLVE_THREADS) {
+      const int comp = l / n2, rem = l - comp * n2;
+      sx[l] = __ldg(x + comp * E.ncomp + psi_index(E, cx, cy, rem / E.n, rem % E.n));
+      sp[l] = __ldg(ipiv + (size_t)e * nb + l);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < nb; ++i) {
+        const int p = sp[i];
+        if (p != i) {
+          const double t = sx[i];
+          sx[i] = sx[p];
+          sx[p] = t;
+        }
       }
     }
   }
   __syncthreads();
-  // forward: unit lower L
+  // (2) forward, unit lower L, 32-row blocks: warp 0 solves the diagonal
+  //     block, then every thread updates one row below it (32 loads in flight)
   for (int b0 = 0; b0 < nb; b0 += 32) {
     const int bs = nb - b0 < 32 ? nb - b0 : 32;
     if (warp == 0) {
+      // diagonal block through shared memory (row-contiguous, coalesced)
+      for (int i = 0; i < bs; ++i)
+        if (lane < bs) sD[i * 33 + lane] = __ldg(L + (size_t)(b0 + i) * nb + b0 + lane);
+      __syncwarp();
       double xi = lane < bs ? sx[b0 + lane] : 0.0;
-      double lr[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        lr[j] = (lane < bs && j < lane) ? __ldg(L + (size_t)(b0 + lane) * nb + b0 + j) : 0.0;
-#pragma unroll
+#pragma unroll 8
       for (int j = 0; j < 32; ++j) {
         const double xj = __shfl_sync(~0u, xi, j);
-        if (j < lane) xi -= lr[j] * xj;
+        if (j < lane && lane < bs) xi -= sD[lane * 33 + j] * xj;
       }
       if (lane < bs) sx[b0 + lane] = xi;
     }
     __syncthreads();
-    const double xl = lane < bs ? sx[b0 + lane] : 0.0;
-#pragma unroll 4
-    for (int i = b0 + bs + warp; i < nb; i += NW) {
-      double s = lane < bs ? __ldg(L + (size_t)i * nb + b0 + lane) * xl : 0.0;
+    for (int i = b0 + bs + tid; i < nb; i += SOLVE_THREADS) {
+      const double* Lr = L + (size_t)i * nb + b0;
+      double s0 = 0.0, s1 = 0.0;
+      if (bs == 32) {
 #pragma unroll
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(~0u, s, off);
-      if (lane == 0) sx[i] -= s;
+        for (int j = 0; j < 32; j += 2) {
+          s0 += __ldg(Lr + j) * sx[b0 + j];
+          s1 += __ldg(Lr + j + 1) * sx[b0 + j + 1];
+        }
+      } else {
+        for (int j = 0; j < bs; ++j) s0 += __ldg(Lr + j) * sx[b0 + j];
+      }
+      sx[i] -= s0 + s1;
     }
     __syncthreads();
   }
-  // backward: upper U (non-unit diagonal)
+  // (3) backward, upper U (non-unit diagonal)
   for (int b0 = ((nb - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
     const int bs = nb - b0 < 32 ? nb - b0 : 32;
     if (warp == 0) {
+      for (int i = 0; i < bs; ++i)
+        if (lane < bs) sD[i * 33 + lane] = __ldg(L + (size_t)(b0 + i) * nb + b0 + lane);
+      __syncwarp();
       double xi = lane < bs ? sx[b0 + lane] : 0.0;
-      double ur[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        ur[j] = (lane < bs && j >= lane && j < bs) ? __ldg(L + (size_t)(b0 + lane) * nb + b0 + j) : 0.0;
-#pragma unroll
-      for (int j = 31; j >= 0; --j) {
-        if (j < bs) {
-          if (lane == j) xi = xi / ur[j];
-          const double xj = __shfl_sync(~0u, xi, j);
-          if (lane < j) xi -= ur[j] * xj;
-        }
+      for (int j = bs - 1; j >= 0; --j) {
+        if (lane == j) xi = xi / sD[j * 33 + j];
+        const double xj = __shfl_sync(~0u, xi, j);
+        if (lane < j) xi -= sD[lane * 33 + j] * xj;
       }
       if (lane < bs) sx[b0 + lane] = xi;
     }
     __syncthreads();
-    const double xl = lane < bs ? sx[b0 + lane] : 0.0;
-#pragma unroll 4
-    for (int i = warp; i < b0; i += NW) {
-      double s = lane < bs ? __ldg(L + (size_t)i * nb + b0 + lane) * xl : 0.0;
+    for (int i = tid; i < b0; i += SOLVE_THREADS) {
+      const double* Ur = L + (size_t)i * nb + b0;
+      double s0 = 0.0, s1 = 0.0;
+      if (bs == 32) {
 #pragma unroll
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(~0u, s, off);
-      if (lane == 0) sx[i] -= s;
+        for (int j = 0; j < 32; j += 2) {
+          s0 += __ldg(Ur + j) * sx[b0 + j];
+          s1 += __ldg(Ur + j + 1) * sx[b0 + j + 1];
+        }
+      } else {
+        for (int j = 0; j < bs; ++j) s0 += __ldg(Ur + j) * sx[b0 + j];
+      }
+      sx[i] -= s0 + s1;
     }
     __syncthreads();
   }
@@ -395,9 +467,164 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_lu_solve(ElemArgs E, const do
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small blocks (nb <= 32, config 4): one warp per block, lane = row, the row
+// in registers; pivots by warp argmax, interchanges and the pivot row by
+// shuffles (same operation order as the CTA kernel's panel loop).
+constexpr int WARP_THREADS = 128;
+
+__device__ __forceinline__ double pivot_mag(double v) {
+  const double m = fabs(v);
+  return m >= 0.0 ? m : -1.0;     // NaN never wins (the block is flagged non-finite)
+}
+
+template <int NBM>
+__global__ void __launch_bounds__(WARP_THREADS, NBM > 16 ? 2 : 4) k_lu_warp(PrecArgs A) {
+  constexpr int NOPIV = 0x7fffffff;
+  const int lane = threadIdx.x & 31;
+  const int nb = A.nb;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int cl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cl < A.count; cl += nw) {
+    double* M = A.M + (size_t)cl * nb * nb;
+    const bool rv = lane < nb;
+    double a[NBM];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < NBM; ++k) {
+      double v = 0.0;
+      if (rv && k < nb) {
+        v = M[lane * nb + k];
+        if (A.transform) v = precond_value(A, A.cell0 + cl, lane, k, v);
+      }
+      a[k] = v;
+      bad |= !isfinite(v);
+    }
+    int info = 0;
+    int prow = lane;                      // composed interchanges (row held by this lane)
+#pragma unroll
+    for (int j = 0; j < NBM; ++j) {
+      if (j < nb) {
+      double best = (rv && lane >= j) ? pivot_mag(a[j]) : -1.0;
+      int bi = (rv && lane >= j && best >= 0.0) ? lane : NOPIV;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double ov = __shfl_xor_sync(~0u, best, off);
+        const int oi = __shfl_xor_sync(~0u, bi, off);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      const int p = bi == NOPIV ? j : bi;
+      if (lane == 0) A.ipiv[(size_t)cl * nb + j] = p;
+      if (p != j) {
+#pragma unroll
+        for (int k = 0; k < NBM; ++k) {
+          const double t1 = __shfl_sync(~0u, a[k], p);
+          const double t2 = __shfl_sync(~0u, a[k], j);
+          if (lane == j) a[k] = t1;
+          else if (lane == p) a[k] = t2;
+        }
+        const int q1 = __shfl_sync(~0u, prow, p);
+        const int q2 = __shfl_sync(~0u, prow, j);
+        if (lane == j) prow = q1;
+        else if (lane == p) prow = q2;
+      }
+      const double pv = __shfl_sync(~0u, a[j], j);
+      if (pv == 0.0) info |= 2;
+      const double rp = 1.0 / pv;
+      if (rv && lane > j && pv != 0.0) a[j] = fabs(pv) >= DBL_MIN ? a[j] * rp : a[j] / pv;
+      const double l = a[j];
+#pragma unroll
+      for (int k = j + 1; k < NBM; ++k) {
+        const double u = __shfl_sync(~0u, a[k], j);
+        if (lane > j) a[k] -= l * u;
+      }
+      }
+    }
+    if (rv) {
+#pragma unroll
+      for (int k = 0; k < NBM; ++k)
+        if (k < nb) M[lane * nb + k] = a[k];
+      if (A.perm != nullptr) A.perm[(size_t)cl * nb + lane] = prow;
+    }
+    const unsigned anybad = __ballot_sync(~0u, bad);
+    if (lane == 0 && A.info && (anybad || info)) atomicOr(A.info, (anybad ? 1 : 0) | info);
+  }
+}
+
+template <int NBM>
+__global__ void __launch_bounds__(WARP_THREADS) k_lu_solve_warp(ElemArgs E, const double* __restrict__ lu,
+                                                                const int* __restrict__ ipiv, int nb,
+                                                                const double* __restrict__ x,
+                                                                double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (e >= E.N) return;
+  const int cx = e / E.ncy, cy = e - cx * E.ncy;
+  const int n2 = E.n * E.n;
+  const bool rv = lane < nb;
+  const double* L = lu + (size_t)e * nb * nb;
+  double r[NBM];
+#pragma unroll
+  for (int k = 0; k < NBM; ++k) r[k] = (rv && k < nb) ? __ldg(L + lane * nb + k) : 0.0;
+  long long gi = 0;
+  double xv = 0.0;
+  int pv = lane;
+  if (rv) {
+    const int comp = lane / n2, rem = lane - comp * n2;
+    gi = comp * E.ncomp + psi_index(E, cx, cy, rem / E.n, rem % E.n);
+    xv = __ldg(x + gi);
+    pv = __ldg(ipiv + (size_t)e * nb + lane);
+  }
+#pragma unroll
+  for (int j = 0; j < NBM; ++j) {
+    if (j >= nb) break;
+    const int p = __shfl_sync(~0u, pv, j);
+    if (p != j) {
+      const double t1 = __shfl_sync(~0u, xv, p);
+      const double t2 = __shfl_sync(~0u, xv, j);
+      if (lane == j) xv = t1;
+      else if (lane == p) xv = t2;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NBM; ++j) {
+    if (j >= nb) break;
+    const double xj = __shfl_sync(~0u, xv, j);
+    if (lane > j) xv -= r[j] * xj;
+  }
+#pragma unroll
+  for (int j = NBM - 1; j >= 0; --j) {
+    if (j < nb) {
+      if (lane == j) xv = xv / r[j];
+      const double xj = __shfl_sync(~0u, xv, j);
+      if (lane < j) xv -= r[j] * xj;
+    }
+  }
+  if (rv) y[gi] = xv;
+}
+
+template <int NBM>
+int launch_lu_warp_t(const PrecArgs& A, int nsm, cudaStream_t s) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lu_warp<NBM>, WARP_THREADS, 0);
+  const long long need = ((long long)A.count * 32 + WARP_THREADS - 1) / WARP_THREADS;
+  const long long cap = (long long)nsm * (occ > 0 ? occ : 1);
+  k_lu_warp<NBM><<<(int)(need < cap ? need : cap), WARP_THREADS, 0, s>>>(A);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HPG_OK : set_error(HPG_ERR_CUDA, "k_lu_warp launch", e);
+}
+
+template <int NBM>
+int launch_lu_solve_warp_t(const ElemArgs& E, const double* lu, const int* ipiv, int nb, const double* x,
+                           double* y, cudaStream_t s) {
+  const int grid = (int)(((long long)E.N * 32 + WARP_THREADS - 1) / WARP_THREADS);
+  k_lu_solve_warp<NBM><<<grid, WARP_THREADS, 0, s>>>(E, lu, ipiv, nb, x, y);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HPG_OK : set_error(HPG_ERR_CUDA, "k_lu_solve_warp launch", e);
+}
+
 template <int KB>
 size_t lu_smem(int nb) {
-  return sizeof(double) * ((size_t)(nb + KB) * (KB + 1) + 2 * KB * LU_ULD + 8) + sizeof(int) * (8 + KB);
+  return sizeof(double) * ((size_t)(nb + KB) * (KB + 1) + 2 * KB * LU_ULD + 8) + sizeof(int) * (8 + 3 * KB + 1 + nb);
 }
 
 template <int KB>
@@ -420,7 +647,7 @@ constexpr size_t LU_SMEM_CAP = 220u << 10;
 
 int lu_max_nb() {
   // the KB = 8 panel is the smallest one
-  return (int)((LU_SMEM_CAP - sizeof(double) * (8 * 9 + 16 * LU_ULD + 8) - sizeof(int) * 16) / (sizeof(double) * 9));
+  return (int)((LU_SMEM_CAP - sizeof(double) * (8 * 9 + 16 * LU_ULD + 8) - sizeof(int) * 33) / (sizeof(double) * 9 + sizeof(int)));
 }
 
 int launch_triple(const double* Zhat, const double* lam_hat, int n, const double* key_hx,
@@ -446,6 +673,9 @@ int launch_precond_transform(const PrecArgs& A, cudaStream_t s) {
 }
 
 int launch_lu(const PrecArgs& A, int nsm, cudaStream_t s) {
+  if (A.nb <= 8) return launch_lu_warp_t<8>(A, nsm, s);
+  if (A.nb <= 16) return launch_lu_warp_t<16>(A, nsm, s);
+  if (A.nb <= 32) return launch_lu_warp_t<32>(A, nsm, s);
   // widest panel that fits shared memory (HPG_LU_KB overrides, for tuning)
   int kb = 32;
   if (const char* env = getenv("HPG_LU_KB")) kb = atoi(env);
@@ -460,14 +690,17 @@ int launch_lu(const PrecArgs& A, int nsm, cudaStream_t s) {
   }
 }
 
-int launch_lu_solve(const ElemArgs& E, const double* lu, const int* ipiv, int nb, const double* x,
-                    double* y, cudaStream_t s) {
-  const size_t smem = (sizeof(double) + sizeof(int)) * (size_t)nb + 16;
+int launch_lu_solve(const ElemArgs& E, const double* lu, const int* ipiv, const int* perm, int nb,
+                    const double* x, double* y, cudaStream_t s) {
+  if (nb <= 8) return launch_lu_solve_warp_t<8>(E, lu, ipiv, nb, x, y, s);
+  if (nb <= 16) return launch_lu_solve_warp_t<16>(E, lu, ipiv, nb, x, y, s);
+  if (nb <= 32) return launch_lu_solve_warp_t<32>(E, lu, ipiv, nb, x, y, s);
+  const size_t smem = (sizeof(double) + sizeof(int)) * (size_t)nb + sizeof(double) * 32 * 33 + 16;
   if (smem > (48u << 10)) {
     cudaError_t e = cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_lu_solve)", e);
   }
-  k_lu_solve<<<E.N, SOLVE_THREADS, smem, s>>>(E, lu, ipiv, nb, x, y);
+  k_lu_solve<<<E.N, SOLVE_THREADS, smem, s>>>(E, lu, ipiv, perm, nb, x, y);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HPG_OK : set_error(HPG_ERR_CUDA, "k_lu_solve launch", e);
 }

@@ -29,15 +29,53 @@ struct PrecArgs {
   double* M;            // blocks, in/out
   int* ipiv;            // [count][nb], 0-based row interchanges (scipy lu_factor)
   int* info;            // device flags: |= 1 non-finite entry, |= 2 exactly zero pivot
+  int* perm;            // optional [count][nb]: composed interchanges, position i <- row perm[i]
+  unsigned long long* prof;  // optional per-phase cycle counters (tools/prof_precond.py)
 };
+
+// spectral mass entry (assembly.py:128-144) and stiffness diagonal (:147-153)
+__device__ __forceinline__ double smass(int a, int c, double h) {
+  if (a == c) return h * (1.0 / (2 * a + 1) + 1.0 / (2 * a + 5));
+  if (a - c == 2 || c - a == 2) return -h / (2 * (a < c ? a : c) + 5);
+  return 0.0;
+}
+__device__ __forceinline__ double sstiff(int a, double h) { return 4.0 * (2.0 * a + 3.0) / h; }
+
+// Entry (row, col) of P_e from D_e's entry v.  tri_e: the cell's triple
+// (obstacle; row-major n2 x n2) or null (gradient).
+__device__ __forceinline__ double precond_entry(int kind, int n, int n2, double hx, double hy,
+                                                double alpha, double beta, const double* tri_e,
+                                                int row, int col, double v) {
+  if (kind == 0) {   // HPG_OBSTACLE
+    double t = -v - tri_e[(size_t)row * n2 + col] / alpha;
+    if (row == col) {
+      const int a = row / n, b = row - (row / n) * n;
+      t -= beta * ((hx / (2.0 * a + 1.0)) * (hy / (2.0 * b + 1.0)));
+    }
+    return t;
+  }
+  double t = -v;
+  if (beta != 0.0) {
+    const int cr = row / n2, cc = col / n2;
+    if (cr == cc) {
+      const int rr = row - cr * n2, c2 = col - cc * n2;
+      const int a = rr / n, b = rr - (rr / n) * n;
+      const int c = c2 / n, d = c2 - (c2 / n) * n;
+      const double e1 = (a == c) ? sstiff(a, hx) * smass(b, d, hy) : 0.0;
+      const double e2 = (b == d) ? smass(a, c, hx) * sstiff(b, hy) : 0.0;
+      t -= beta * (e1 + e2);
+    }
+  }
+  return t;
+}
 
 // host-side launchers (hpg_precond.cu)
 int launch_triple(const double* Zhat, const double* lam_hat, int n, const double* key_hx,
                   const double* key_hy, int nkeys, double* tri, cudaStream_t s);
 int launch_precond_transform(const PrecArgs& A, cudaStream_t s);
 int launch_lu(const PrecArgs& A, int nsm, cudaStream_t s);
-int launch_lu_solve(const ElemArgs& E, const double* lu, const int* ipiv, int nb, const double* x,
-                    double* y, cudaStream_t s);
+int launch_lu_solve(const ElemArgs& E, const double* lu, const int* ipiv, const int* perm, int nb,
+                    const double* x, double* y, cudaStream_t s);
 int lu_max_nb();
 
 }  // namespace hpg

@@ -305,6 +305,13 @@ class _DeviceDisc:
         if beta < 0:
             raise ValueError("beta must be >= 0")
         self._precond_ready()
+        nb = self.n * self.n * self.ncomp
+        if isinstance(D, DeviceCellBlockMatrix):
+            # fused: the blocks kernel writes P_e directly from D's point weights
+            out = torch.empty((self.plan.ncells, nb, nb), dtype=F64, device=self.device)
+            _lib.call("hpgPrecondAssemble", self.plan.handle, _vp(D._w), float(alpha), float(beta),
+                      _vp(out), 0, self.plan.ncells, _stream())
+            return out
         out = self._blocks_of(D)
         _lib.call("hpgPrecondBlocks", self.plan.handle, _vp(out), float(alpha), float(beta), 0,
                   self.plan.ncells, _stream())
@@ -568,10 +575,11 @@ class DeviceCellBlockPreconditioner:
     ``(lu, piv)`` host pairs on demand.
     """
 
-    def __init__(self, disc, lu_t, piv_t, info_t=None, check=True):
+    def __init__(self, disc, lu_t, piv_t, info_t=None, check=True, perm_t=None):
         self.disc = disc
         self.lu_t = lu_t
         self.piv_t = piv_t
+        self.perm_t = perm_t
         self.info_t = info_t
         self.n = disc.ndof_psi
         self._factors = None
@@ -594,12 +602,21 @@ class DeviceCellBlockPreconditioner:
         if beta < 0:
             raise ValueError("beta must be >= 0")
         disc._precond_ready()
-        lu = disc._blocks_of(D)
-        piv = torch.empty(lu.shape[:2], dtype=torch.int32, device=disc.device)
         info = torch.zeros(1, dtype=torch.int32, device=disc.device)
-        _lib.call("hpgPrecondFactor", disc.plan.handle, _vp(lu), _vp(piv), float(alpha), float(beta),
-                  0, disc.plan.ncells, _vp(info), _stream())
-        return cls(disc, lu, piv, info)
+        if isinstance(D, DeviceCellBlockMatrix):
+            # P_e written by the blocks kernel's epilogue, then factored in place
+            lu = disc.precond_blocks_t(D, alpha, beta)
+            piv = torch.empty(lu.shape[:2], dtype=torch.int32, device=disc.device)
+            perm = torch.empty_like(piv)
+            _lib.call("hpgLUFactor", disc.plan.handle, _vp(lu), _vp(piv), _vp(perm), disc.plan.ncells,
+                      _vp(info), _stream())
+        else:
+            lu = disc._blocks_of(D)
+            piv = torch.empty(lu.shape[:2], dtype=torch.int32, device=disc.device)
+            perm = torch.empty_like(piv)
+            _lib.call("hpgPrecondFactor", disc.plan.handle, _vp(lu), _vp(piv), _vp(perm), float(alpha),
+                      float(beta), 0, disc.plan.ncells, _vp(info), _stream())
+        return cls(disc, lu, piv, info, perm_t=perm)
 
     @classmethod
     def from_blocks(cls, disc, blocks):
@@ -613,10 +630,11 @@ class DeviceCellBlockPreconditioner:
         if lu.shape != (disc.plan.ncells, nb, nb):
             raise ValueError("blocks have the wrong shape")
         piv = torch.empty(lu.shape[:2], dtype=torch.int32, device=disc.device)
+        perm = torch.empty_like(piv)
         info = torch.zeros(1, dtype=torch.int32, device=disc.device)
-        _lib.call("hpgLUFactor", disc.plan.handle, _vp(lu), _vp(piv), disc.plan.ncells, _vp(info),
-                  _stream())
-        return cls(disc, lu, piv, info)
+        _lib.call("hpgLUFactor", disc.plan.handle, _vp(lu), _vp(piv), _vp(perm), disc.plan.ncells,
+                  _vp(info), _stream())
+        return cls(disc, lu, piv, info, perm_t=perm)
 
     @property
     def indices(self):
@@ -634,8 +652,8 @@ class DeviceCellBlockPreconditioner:
         d = self.disc
         d._check_len(x_t, self.n, "x")
         out = torch.empty(self.n, dtype=F64, device=d.device) if out is None else out
-        _lib.call("hpgLUSolve", d.plan.handle, _vp(self.lu_t), _vp(self.piv_t), _vp(x_t), _vp(out),
-                  _stream())
+        _lib.call("hpgLUSolve", d.plan.handle, _vp(self.lu_t), _vp(self.piv_t), _vp(self.perm_t),
+                  _vp(x_t), _vp(out), _stream())
         return out
 
     def apply(self, x):

@@ -30,7 +30,14 @@ def test_precond_blocks_and_apply_golden(name):
         with pytest.raises(ValueError):
             d.schur_preconditioner(D, g["alpha"], beta)
         return
-    pb = d.precond_blocks(D, g["alpha"], beta)
+    pb = d.precond_blocks(D, g["alpha"], beta)          # fused into the blocks kernel
+    if g["p"] < 82:
+        # from a host CellBlockMatrix-like D (hpgPrecondBlocks transform path)
+        from types import SimpleNamespace
+        pb_host = d.precond_blocks(SimpleNamespace(blocks=D.blocks), g["alpha"], beta)
+        assert orc.rel_err(np.stack(pb_host), np.stack(pb)) < 1e-15
+        M3 = DeviceCellBlockPreconditioner.from_operator(d, SimpleNamespace(blocks=D.blocks), g["alpha"], beta) \
+            if np.isfinite(g["precond_apply"]).all() else None
     if "precond_blocks" in g:
         assert orc.rel_err(np.stack(pb), g["precond_blocks"]) < TOL
     else:
@@ -45,6 +52,8 @@ def test_precond_blocks_and_apply_golden(name):
     # from materialised blocks, as CellBlockPreconditioner(blocks, ...)
     M2 = DeviceCellBlockPreconditioner.from_blocks(d, pb)
     assert orc.rel_err(M2.apply(g["x"]), g["precond_apply"]) < TOL
+    if M3 is not None:                                  # fused transform + LU (hpgPrecondFactor)
+        assert orc.rel_err(M3.apply(g["x"]), g["precond_apply"]) < TOL
 
 
 @pytest.mark.parametrize("kind,p", [("obstacle", 2), ("obstacle", 4), ("obstacle", 8),
@@ -130,3 +139,30 @@ def test_lu_unsupported_size_is_loud():
     D = d.assemble_D_t(dev["psi"])
     with pytest.raises(_lib.HpgError):
         d.schur_preconditioner(D, 1.0, 0.0)
+
+
+@pytest.mark.parametrize("kind,p", [("obstacle", 4), ("obstacle", 16), ("gradient", 6)])
+def test_composed_permutation(kind, p):
+    """perm (position i <- row perm[i]) equals LAPACK's swaps replayed; the
+    solve gives the same result with perm and with ipiv only."""
+    import torch
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    cls = D.ObstacleDisc2D if kind == "obstacle" else D.GradientDisc2D
+    d = cls(uniform_mesh_2d(0.0, 1.0, 2, p), 1.0, 0.5, rule="gauss", nq=p + 2)
+    nb = d.n * d.n * d.ncomp
+    rng = np.random.default_rng(7)
+    blocks = rng.standard_normal((d.plan.ncells, nb, nb))
+    M = D.DeviceCellBlockPreconditioner.from_blocks(d, list(blocks))
+    piv = M.piv_t.cpu().numpy()
+    perm = M.perm_t.cpu().numpy()
+    for i in range(d.plan.ncells):
+        ref = np.arange(nb)
+        for j, q in enumerate(piv[i]):
+            ref[[j, q]] = ref[[q, j]]
+        assert np.array_equal(perm[i], ref)
+    x = torch.from_numpy(rng.standard_normal(d.ndof_psi)).cuda()
+    y1 = M.apply_t(x).cpu().numpy()
+    M.perm_t = None
+    y2 = M.apply_t(x).cpu().numpy()
+    assert orc.rel_err(y1, y2) < 1e-14
