@@ -213,6 +213,41 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm):
+    """Factor (P blocks + LU) and apply (per-cell solves) of the device
+    CellBlockPreconditioner at beta = 1e-8 (the CLI default, cli.py:142)."""
+    import torch
+    from paper_2412_13733_b200.disc import DeviceCellBlockPreconditioner
+    alpha, beta = cfg.alphas[-1], 1e-8
+    disc.residual_t(alpha, psi_prev, u, psi, b_u=b_u, b_psi=b_psi, flag=flag, wcache=True)
+    D = disc.assemble_D_t(psi)
+    M = DeviceCellBlockPreconditioner.from_operator(disc, D, alpha, beta)
+    y = M.apply_t(x)
+    torch.cuda.synchronize()
+    N, nb = disc.plan.ncells, cfg.ncomp * disc.n * disc.n
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    reps_f, reps_a = 3, 20
+    ev[0].record()
+    for _ in range(reps_f):
+        M = DeviceCellBlockPreconditioner.from_operator(disc, D, alpha, beta)
+    ev[1].record()
+    ev[2].record()
+    for _ in range(reps_a):
+        M.apply_t(x, out=y)
+    ev[3].record()
+    torch.cuda.synchronize()
+    t_f = ev[0].elapsed_time(ev[1]) * 1e-3 / reps_f
+    t_a = ev[2].elapsed_time(ev[3]) * 1e-3 / reps_a
+    F_f = N * 2.0 / 3.0 * nb ** 3
+    B_f = 16.0 * N * nb * nb            # P written by the assembly epilogue, LU read+written once
+    B_a = 8.0 * N * nb * nb + 16.0 * disc.ndof_psi
+    lb_f = max(F_f / (P_FP64_TFLOPS * 1e12), B_f / (hbm * 1e9))
+    return {"beta": beta, "factor_ms": t_f * 1e3, "factor_tflops": F_f / t_f / 1e12,
+            "factor_roofline_frac": lb_f / t_f, "apply_us": t_a * 1e6, "apply_gbs": B_a / t_a / 1e9,
+            "apply_roofline_frac": (B_a / (hbm * 1e9)) / t_a, "nb": nb,
+            "path": "hpgPrecondAssemble + hpgLUFactor (from_operator), hpgLUSolve (apply)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -420,6 +455,13 @@ def main():
                   "roofline_frac": t_lb / t_blk, "bytes": B_blk, "flops": F_blk}
         del out_blk
 
+    # per-cell Schur preconditioner (not part of the
+    # headline workload): P blocks from the cached weights, batched LU, solve
+    from paper_2412_13733_b200 import _lib
+    precond = None
+    if world == 1 and cfg.ncomp * disc.n * disc.n <= _lib.load().hpgLUMaxBlock():
+        precond = precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -440,6 +482,7 @@ def main():
             "roofline": roof,
             "step_roofline_frac": step_frac,
             "blocks": blocks,
+            "precond": precond,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
