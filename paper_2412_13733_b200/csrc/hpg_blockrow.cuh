@@ -141,6 +141,10 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
       if (B.per_warp) __syncwarp(); else __syncthreads();
       // contiguous block row (a*n + b): entries j*n + k, coalesced across the group
       const long long row = (long long)a * n + b;
+      // fused precond epilogue (obstacle): P = -D - T/alpha - beta mass on the diagonal
+      const double* trow = (B.prec && B.nf == 1) ? B.tri + ((size_t)B.key[e] * n2 + row) * n2 : nullptr;
+      const double ainv = B.prec ? 1.0 / B.alpha : 0.0;
+      const double dmass = B.prec ? B.beta * ((B.hx[cx] / (2.0 * a + 1.0)) * (B.hy[cy] / (2.0 * b + 1.0))) : 0.0;
       const int gt = B.per_warp ? lane : threadIdx.x, gn = B.per_warp ? 32 : blockDim.x;
       int j = gt / n, k = gt - (gt / n) * n;                 // (j, k) of idx, advanced incrementally
       const int dj = gn / n, dk = gn - (gn / n) * n;
@@ -149,9 +153,15 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
         j += dj;
         k += dk;
         if (k >= n) { k -= n; ++j; }
-        if (B.nf == 1 || f == 0) {
-          blk[row * B.nb + idx] = B.prec ? precond_entry(B.nf == 1 ? 0 : 1, n, (int)n2, B.hx[cx], B.hy[cy], B.alpha,
-                                                         B.beta, B.nf == 1 ? B.tri + (size_t)B.key[e] * n2 * n2 : nullptr,
+        if (B.nf == 1) {
+          double w = v;
+          if (B.prec) {
+            w = -v - trow[idx] * ainv;
+            if (idx == row) w -= dmass;
+          }
+          blk[row * B.nb + idx] = w;
+        } else if (f == 0) {
+          blk[row * B.nb + idx] = B.prec ? precond_entry(1, n, (int)n2, B.hx[cx], B.hy[cy], B.alpha, B.beta, nullptr,
                                                          (int)row, idx, v)
                                          : v;
         } else if (f == 1) {
