@@ -160,6 +160,20 @@ int hpgLUMaxBlock(void);
  * phase into (NULL disables; off by default). */
 int hpgLUProfile(unsigned long long* counters);
 
+/* Interior stiffness solve by fast diagonalisation (
+ * replaces linalg.factor_stiffness / SpluFactor.solve, linalg.py:100-117, for
+ * A = Kx(x)My + Mx(x)Ky, assembly.py:42-78, 470-474).  HOST inputs: the 1D
+ * generalized eigenpairs Kx Vx = Mx Vx diag(lx), Vx^T Mx Vx = I (nix x nix
+ * row-major, nix) and the same in y (schur.py: u_matrices_1d + eigh).
+ * hpgStiffnessSolve: x = A^{-1} b on interior U vectors (four cuBLAS DGEMMs).
+ * hpgSchurApply: SchurOperator.matvec (linalg.py:223-229) in one call,
+ *   y = -((D x + E_beta x) + B^T A^{-1} B x / alpha), D from cached weights. */
+int hpgStiffnessFactor(hpgPlan plan, const double* Vx, const double* lx,
+                       const double* Vy, const double* ly, void* stream);
+int hpgStiffnessSolve(hpgPlan plan, const double* b, double* x, void* stream);
+int hpgSchurApply(hpgPlan plan, const double* wcache, double alpha,
+                  double beta, const double* x, double* y, void* stream);
+
 const char* hpgLastError(void);
 int hpgVersion(void);
 

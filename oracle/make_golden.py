@@ -36,6 +36,7 @@ from paper_2412_13733_b200.workloads import (make_inputs, phi_bilinear,  # noqa:
                                              phi_sin)
 
 PREC_BETA = 0.25     # large enough that the E_beta term shows in the parity checks
+SCHUR_RTOL = 1e-10
 OUT = os.path.join(os.path.dirname(__file__), "..", "tests", "golden")
 
 
@@ -77,7 +78,7 @@ def build(kind, xpts, ypts, p, rule, Q, f, phi):
 
 
 def case(name, kind, xpts, ypts, p, rule, Q=None, alpha=1.0, phi=phi_sin,
-         seed=0, psi_scale=1.0, block_rows=None, psi_override=None):
+         seed=0, psi_scale=1.0, block_rows=None, psi_override=None, schur=True):
     xpts = np.asarray(xpts, dtype=float)
     ypts = np.asarray(ypts, dtype=float)
     disc, t = build(kind, xpts, ypts, p, rule, Q, 1.0, phi)
@@ -109,6 +110,16 @@ def case(name, kind, xpts, ypts, p, rule, Q=None, alpha=1.0, phi=phi_sin,
         out["precond_apply"] = linalg.schur_preconditioner(disc, D, alpha, PREC_BETA).apply(x)
     except ValueError:          # scipy lu_factor rejects non-finite blocks
         out["precond_error"] = True
+    # Schur-reduced Newton step (linalg.py:213-287) with SuperLU on A
+    if schur and not np.isnan(psi).any():
+        A_factor = linalg.factor_stiffness(disc.A, "splu", 2)
+        E = disc.E_matrix(PREC_BETA)
+        out["stiff_solve"] = A_factor.solve(u)
+        out["schur_mv"] = linalg.SchurOperator(disc, D, E, alpha, A_factor).matvec(x)
+        r = linalg.schur_solve(disc, D, alpha, PREC_BETA, out["b_u"], out["b_psi"], A_factor,
+                               rtol=SCHUR_RTOL, maxiter=150, E=E)
+        out.update(schur_du=r.du, schur_dpsi=r.dpsi, schur_iters=r.gmres.iterations,
+                   schur_res=np.asarray(r.gmres.residuals))
     if block_rows is None:
         out["blocks"] = blocks
         out["precond_blocks"] = pb
@@ -148,16 +159,16 @@ def main():
     case("grad_p6_gauss", "gradient", u2, u2, 6, "gauss", Q=9, phi=phi_bilinear)
     # config 3 degree on one cell, blocks as selected rows
     case("c3_ref", "obstacle", u1, u1, 82, "reference",
-         block_rows=np.array([0, 1, 80, 81, 3280, 6560]))
+         block_rows=np.array([0, 1, 80, 81, 3280, 6560]), schur=False)
     case("c3_gauss", "obstacle", u1, u1, 82, "gauss", Q=128,
-         block_rows=np.array([0, 1, 80, 81, 3280, 6560]))
+         block_rows=np.array([0, 1, 80, 81, 3280, 6560]), schur=False)
     # non-uniform widths, rectangular mesh
     xs = np.array([0.0, 0.15, 0.5, 1.0])
     ys = np.array([0.0, 0.3, 1.0])
     case("nonuni_ref", "obstacle", xs, ys, 5, "reference", alpha=2.0)
     case("nonuni_grad_gauss", "gradient", xs, ys, 4, "gauss", Q=7, phi=phi_bilinear)
     # clamp: overflow side must flag; NaN must flag
-    case("clamp_ref", "obstacle", u2, u2, 3, "reference", psi_scale=-2000.0)
+    case("clamp_ref", "obstacle", u2, u2, 3, "reference", psi_scale=-2000.0, schur=False)
 
     def nan_one(psi):
         psi = psi.copy()

@@ -45,6 +45,9 @@ SIGNATURES = {
     "hpgLUSolve": [_P, _P, _P, _P, _P, _P, _P],
     "hpgLUMaxBlock": [],
     "hpgLUProfile": [_P],
+    "hpgStiffnessFactor": [_P, _P, _P, _P, _P, _P],
+    "hpgStiffnessSolve": [_P, _P, _P, _P],
+    "hpgSchurApply": [_P, _P, _D, _D, _P, _P, _P],
     "hpgVersion": [],
 }
 

@@ -14,6 +14,9 @@
 #include "hpg_common.cuh"
 #include "hpg_launch.cuh"
 #include "hpg_precond.cuh"
+#include "hpg_schur.cuh"
+
+#include <cublas_v2.h>
 #include "hpg_useside.cuh"
 #include "hpg_small.cuh"
 #include "hpg_ucell.cuh"
@@ -97,6 +100,12 @@ struct hpgPlan_st {
   double* tri = nullptr;         // [nkeys][n2][n2]
   int* cell_key = nullptr;       // [N]
   int nkeys = 0;
+
+  // fast-diagonalisation stiffness solve + Schur apply scratch
+  cublasHandle_t cub = nullptr;
+  double *Vx = nullptr, *Vy = nullptr, *finv = nullptr, *fw1 = nullptr, *fw2 = nullptr;
+  double *su1 = nullptr, *su2 = nullptr, *syD = nullptr, *sz = nullptr;
+  bool fdm_ready = false;
 
   int zcells = 0;
   int* dflag = nullptr;
@@ -286,6 +295,9 @@ int hpgPlanDestroy(hpgPlan P) {
   cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
   cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag); cudaFree(P->edge); cudaFree(P->PKG); cudaFree(P->ubuf);
   cudaFree(P->tri); cudaFree(P->cell_key);
+  cudaFree(P->Vx); cudaFree(P->Vy); cudaFree(P->finv); cudaFree(P->fw1); cudaFree(P->fw2);
+  cudaFree(P->su1); cudaFree(P->su2); cudaFree(P->syD); cudaFree(P->sz);
+  if (P->cub) cublasDestroy(P->cub);
   delete P;
   return HPG_OK;
 }
@@ -736,6 +748,96 @@ int hpgLUMaxBlock(void) { return lu_max_nb(); }
 
 int hpgLUProfile(unsigned long long* counters) {
   g_lu_prof = counters;
+  return HPG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fast-diagonalisation stiffness solve and the Schur operator (linalg.py:100-117, 213-229)
+
+#define CUBLAS_TRY(x)                                                                   \
+  do {                                                                                  \
+    cublasStatus_t _st = (x);                                                           \
+    if (_st != CUBLAS_STATUS_SUCCESS)                                                   \
+      return fail(HPG_ERR_CUDA, std::string(#x) + ": cublas status " + std::to_string((int)_st)); \
+  } while (0)
+
+int hpgStiffnessFactor(hpgPlan P, const double* Vx, const double* lx, const double* Vy, const double* ly,
+                       void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!Vx || !lx || !Vy || !ly) return fail(HPG_ERR_ARG, "null eigen-factors");
+  const long long nix = P->nix, niy = P->niy;
+  if (nix <= 0 || niy <= 0) return fail(HPG_ERR_ARG, "mesh has no interior U dofs");
+  (void)stream;
+  if (P->cub == nullptr) CUBLAS_TRY(cublasCreate(&P->cub));
+  std::vector<double> finv((size_t)nix * niy);
+  for (long long i = 0; i < nix; ++i)
+    for (long long j = 0; j < niy; ++j) finv[(size_t)(i * niy + j)] = 1.0 / (lx[i] + ly[j]);
+  cudaFree(P->Vx); cudaFree(P->Vy); cudaFree(P->finv); cudaFree(P->fw1); cudaFree(P->fw2);
+  cudaFree(P->su1); cudaFree(P->su2); cudaFree(P->syD); cudaFree(P->sz);
+  P->Vx = P->Vy = P->finv = P->fw1 = P->fw2 = P->su1 = P->su2 = P->syD = P->sz = nullptr;
+  P->fdm_ready = false;
+  int rc;
+  if ((rc = upload(&P->Vx, Vx, (size_t)(nix * nix)))) return rc;
+  if ((rc = upload(&P->Vy, Vy, (size_t)(niy * niy)))) return rc;
+  if ((rc = upload(&P->finv, finv.data(), finv.size()))) return rc;
+  CUDA_TRY(cudaMalloc(&P->fw1, sizeof(double) * nix * niy + 16));
+  CUDA_TRY(cudaMalloc(&P->fw2, sizeof(double) * nix * niy + 16));
+  CUDA_TRY(cudaMalloc(&P->su1, sizeof(double) * P->ndof_u + 16));
+  CUDA_TRY(cudaMalloc(&P->su2, sizeof(double) * P->ndof_u + 16));
+  CUDA_TRY(cudaMalloc(&P->syD, sizeof(double) * P->ndof_psi + 16));
+  CUDA_TRY(cudaMalloc(&P->sz, sizeof(double) * P->ndof_psi + 16));
+  P->fdm_ready = true;
+  return HPG_OK;
+}
+
+// row-major C (M x N) = op(A) op(B) through column-major cuBLAS
+static int rm_gemm(hpgPlan P, bool ta, bool tb, int M, int N, int K, const double* A, int lda, const double* B,
+                   int ldb, double* C, int ldc) {
+  const double one = 1.0, zero = 0.0;
+  CUBLAS_TRY(cublasDgemm(P->cub, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K, &one,
+                         B, ldb, A, lda, &zero, C, ldc));
+  return HPG_OK;
+}
+
+static int stiffness_solve(hpgPlan P, const double* b, double* x, cudaStream_t s) {
+  const int nix = P->nix, niy = P->niy;
+  CUBLAS_TRY(cublasSetStream(P->cub, s));
+  int rc;
+  if ((rc = rm_gemm(P, true, false, nix, niy, nix, P->Vx, nix, b, niy, P->fw1, niy))) return rc;        // Vx^T B
+  if ((rc = rm_gemm(P, false, false, nix, niy, niy, P->fw1, niy, P->Vy, niy, P->fw2, niy))) return rc;  // . Vy
+  const long long n = (long long)nix * niy;
+  k_fdm_scale<<<(int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16), 256, 0, s>>>(P->fw2, P->finv, n);
+  LAUNCH_CHECK();
+  if ((rc = rm_gemm(P, false, false, nix, niy, nix, P->Vx, nix, P->fw2, niy, P->fw1, niy))) return rc;  // Vx .
+  return rm_gemm(P, false, true, nix, niy, niy, P->fw1, niy, P->Vy, niy, x, niy);                        // . Vy^T
+}
+
+int hpgStiffnessSolve(hpgPlan P, const double* b, double* x, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!P->fdm_ready) return fail(HPG_ERR_ARG, "hpgStiffnessFactor has not been called on this plan");
+  if (!b || !x) return fail(HPG_ERR_ARG, "null pointer");
+  if (b == x) return fail(HPG_ERR_ARG, "in-place stiffness solve is not supported");
+  return stiffness_solve(P, b, x, (cudaStream_t)stream);
+}
+
+int hpgSchurApply(hpgPlan P, const double* wcache, double alpha, double beta, const double* x, double* y,
+                  void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!P->fdm_ready) return fail(HPG_ERR_ARG, "hpgStiffnessFactor has not been called on this plan");
+  if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  if (x == y) return fail(HPG_ERR_ARG, "in-place Schur apply is not supported");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  if ((rc = hpgApplyCached(P, wcache, x, P->syD, stream))) return rc;   // D x
+  if ((rc = hpgBPsi(P, x, P->su1, stream))) return rc;                  // B x
+  if ((rc = stiffness_solve(P, P->su1, P->su2, s))) return rc;          // A^{-1} B x
+  if ((rc = hpgBTu(P, P->su2, P->sz, stream))) return rc;               // B^T A^{-1} B x
+  ElemArgs A = base_args(P);
+  const long long total = P->ndof_psi;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 148 * 16) grid = 148 * 16;
+  k_schur_combine<<<grid, 256, 0, s>>>(A, P->kind == HPG_GRADIENT, alpha, beta, x, P->syD, P->sz, y);
+  LAUNCH_CHECK();
   return HPG_OK;
 }
 
