@@ -248,6 +248,48 @@ def precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm):
             "path": "hpgPrecondAssemble + hpgLUFactor (from_operator), hpgLUSolve (apply)"}
 
 
+def schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag):
+    """Stiffness solve (fast diagonalisation), one-call Schur apply and one
+    full schur_solve (device preconditioner, GMRES rtol 1e-8) at beta = 1e-8."""
+    import torch
+    from paper_2412_13733_b200 import schur
+    alpha, beta = cfg.alphas[-1], 1e-8
+    Af = schur.DeviceStiffnessFactor(disc)
+    bu, bp, _ = disc.residual_t(alpha, psi_prev, u, psi, b_u=b_u, b_psi=b_psi, flag=flag, wcache=True)
+    D = disc.assemble_D_t(psi)
+    S = schur.DeviceSchurOperator(disc, D, beta, alpha, Af)
+    M = disc.schur_preconditioner(D, alpha, beta)
+    xs = torch.empty_like(u)
+    ys = torch.empty_like(psi)
+    out = {}
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / reps
+
+    t_solve = timed(lambda: Af.solve_t(u, out=xs), 10)
+    t_apply = timed(lambda: S.matvec_t(psi, out=ys), 10)
+
+    def full():
+        out["r"] = schur.schur_solve_t(disc, D, alpha, beta, bu, bp, Af, rtol=1e-8, precond=M)
+
+    t_full = timed(full, 2)
+    nix = cfg.ncells * cfg.p - 1
+    fl = 4 * 2.0 * nix ** 3
+    return {"beta": beta, "stiffness_solve_us": t_solve * 1e6, "stiffness_solve_tflops": fl / t_solve / 1e12,
+            "schur_apply_us": t_apply * 1e6, "schur_solve_ms": t_full * 1e3,
+            "gmres_iterations": out["r"].gmres.iterations,
+            "path": "hpgStiffnessSolve (fast diagonalisation, cuBLAS DGEMM), hpgSchurApply, "
+                    "schur.schur_solve_t (device GMRES + hpgLUSolve), preconditioner factor excluded"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -462,6 +504,11 @@ def main():
     if world == 1 and cfg.ncomp * disc.n * disc.n <= _lib.load().hpgLUMaxBlock():
         precond = precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm)
 
+    # Schur-reduced Newton linear solve on the device
+    schur_info = None
+    if world == 1 and disc.plan.ndof_u > 0:
+        schur_info = schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -483,6 +530,7 @@ def main():
             "step_roofline_frac": step_frac,
             "blocks": blocks,
             "precond": precond,
+            "schur": schur_info,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
