@@ -134,6 +134,28 @@ def case(name, kind, xpts, ypts, p, rule, Q=None, alpha=1.0, phi=phi_sin,
           f"ndof_u={u.size} nq={t.nq} clamped={out['clamped']}")
 
 
+def solve_case(name, kind, nc, p, rule, Q=None, phi=phi_sin, beta=1e-3, alpha_max=8.0,
+               line_search=False):
+    """The reference's whole penalty continuation (proximal.solve) from zero."""
+    pts = np.linspace(0.0, 1.0, nc + 1)
+    disc, t = build(kind, pts, pts, p, rule, Q, 1.0, phi)
+    sched = proximal.AlphaSchedule(alpha0=1.0, rate=2.0, alpha_max=alpha_max)
+    opts = proximal.SolverOptions(line_search=line_search)
+    rep = proximal.solve(disc, sched, beta, opts)
+    out = dict(kind=kind, xpts=pts, ypts=pts, p=p, rule=rule, nq=t.nq, alpha=1.0, beta=beta,
+               alpha_max=alpha_max, line_search=line_search,
+               S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi,
+               u=rep.u, psi=rep.psi, multiplier=rep.multiplier,
+               outer_increment=rep.outer_increment, converged=rep.converged,
+               newton_iters=np.array([s.newton_iters for s in rep.steps]),
+               gmres_iters=np.array([sum(s.gmres_iters) for s in rep.steps]),
+               alphas=np.array([s.alpha for s in rep.steps]))
+    path = os.path.join(OUT, "solve", f"{name}.npz")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    np.savez_compressed(path, **out)
+    print(f"solve/{name}: newton {out['newton_iters'].tolist()} gmres {out['gmres_iters'].tolist()}")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     u4 = np.linspace(0.0, 1.0, 5)
@@ -176,6 +198,10 @@ def main():
         return psi
 
     case("nan_ref", "obstacle", u2, u2, 3, "reference", psi_override=nan_one)
+    # whole continuations (proximal.solve)
+    solve_case("obst_p6_gauss", "obstacle", 4, 6, "gauss", Q=9)
+    solve_case("obst_p8_ref", "obstacle", 4, 8, "reference")
+    solve_case("obst_p4_ls", "obstacle", 6, 4, "gauss", Q=7, line_search=True)
 
 
 if __name__ == "__main__":

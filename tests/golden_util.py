@@ -22,3 +22,21 @@ def load(name):
     for k in ("clamped", "res_clamped", "D_clamped"):
         d[k] = bool(d[k])
     return d
+
+
+def solve_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "solve", "*.npz")))
+
+
+def load_solve(name):
+    with np.load(os.path.join(GOLDEN, "solve", name + ".npz"), allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    for k in ("kind", "rule"):
+        d[k] = str(d[k])
+    for k in ("p", "nq"):
+        d[k] = int(d[k])
+    for k in ("beta", "alpha_max", "outer_increment"):
+        d[k] = float(d[k])
+    d["line_search"] = bool(d["line_search"])
+    d["converged"] = bool(d["converged"])
+    return d
