@@ -174,6 +174,27 @@ int hpgStiffnessSolve(hpgPlan plan, const double* b, double* x, void* stream);
 int hpgSchurApply(hpgPlan plan, const double* wcache, double alpha,
                   double beta, const double* x, double* y, void* stream);
 
+/* QVI temperature operators on the FULL U space (
+ * qvi.py:35-127: _cell_grid_values, _load_full, TemperatureSolver).
+ * hpgUFullSetup (HOST tables): SR = Su R (nq x m), TR = R^T diag(1/(2l+1)) Tu
+ *   (m x nq), Kh / Mh reference-cell stiffness and mass (m x m), and the 1D
+ *   generalized eigenpairs of the full-space stiffness/mass (for H^{-1}).
+ * hpgUFullValues: per-cell (nq x nq) samples of a full U vector.
+ * hpgUFullOperator: out = H v - load(w .* values(v) + rhs),
+ *   H = Kx(x)My + Mx(x)Ky + gamma Mx(x)My; v, w, rhs nullable (0): the
+ *   Newton residual (w = NULL, rhs = g(gap)) or the Jacobian (rhs = NULL).
+ * hpgUFullSolve: x = H^{-1} b (fast diagonalisation; the reference factors H
+ *   with SuperLU and uses it as the left preconditioner). */
+int hpgUFullSetup(hpgPlan plan, double gamma, const double* SR, const double* TR,
+                  const double* Kh, const double* Mh, const double* Vx,
+                  const double* lx, const double* Vy, const double* ly,
+                  void* stream);
+int hpgUFullValues(hpgPlan plan, const double* v, double* vals, void* stream);
+int hpgUFullOperator(hpgPlan plan, double gamma, const double* v,
+                     const double* w, const double* rhs, double* out,
+                     void* stream);
+int hpgUFullSolve(hpgPlan plan, const double* b, double* x, void* stream);
+
 const char* hpgLastError(void);
 int hpgVersion(void);
 

@@ -156,6 +156,32 @@ def solve_case(name, kind, nc, p, rule, Q=None, phi=phi_sin, beta=1e-3, alpha_ma
     print(f"solve/{name}: newton {out['newton_iters'].tolist()} gmres {out['gmres_iters'].tolist()}")
 
 
+def qvi_case(name, nc, p, rule, Q=None, load=100.0, scale=0.05):
+    """QVI temperature pieces (qvi.py:35-127) from the reference's own code."""
+    from hpgalerkin import qvi
+    from hpgalerkin.problems import ThermoformingData
+    data = ThermoformingData(load=load)
+    pts = np.linspace(0.0, 1.0, nc + 1)
+    disc, t = build("obstacle", pts, pts, p, rule, Q, data.f, 0.0)
+    solver = qvi.TemperatureSolver(disc, data)
+    rng = np.random.default_rng(11)
+    nf = solver.H.shape[0]
+    vfull = rng.standard_normal(nf)
+    rvals = rng.standard_normal((len(disc.cell_ids), t.nq, t.nq))
+    _, u, _, _ = make_inputs("obstacle", nc, nc, p, seed=3)
+    u_full = disc.u_space.extend_interior(scale * u)
+    T, newton, gmres_its = solver.solve(u_full)
+    out = dict(xpts=pts, ypts=pts, p=p, rule=rule, nq=t.nq, load=load, gamma=data.gamma,
+               S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi,
+               vfull=vfull, vals=np.stack(qvi._cell_grid_values(disc, vfull)),
+               rvals=rvals, load_full=qvi._load_full(disc, list(rvals)), Hv=solver.H @ vfull,
+               u_full=u_full, temp=T, newton=newton, gmres=np.array(gmres_its))
+    path = os.path.join(OUT, "qvi", f"{name}.npz")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    np.savez_compressed(path, **out)
+    print(f"qvi/{name}: nfull={nf} newton={newton} gmres={gmres_its}")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     u4 = np.linspace(0.0, 1.0, 5)
@@ -198,6 +224,10 @@ def main():
         return psi
 
     case("nan_ref", "obstacle", u2, u2, 3, "reference", psi_override=nan_one)
+    # QVI temperature solve pieces
+    qvi_case("qvi_p4_gauss", 4, 4, "gauss", Q=7)
+    qvi_case("qvi_p6_ref", 3, 6, "reference")
+    qvi_case("qvi_p8_gauss", 4, 8, "gauss", Q=12, scale=0.2)
     # whole continuations (proximal.solve)
     solve_case("obst_p6_gauss", "obstacle", 4, 6, "gauss", Q=9)
     solve_case("obst_p8_ref", "obstacle", 4, 8, "reference")

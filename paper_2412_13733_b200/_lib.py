@@ -48,6 +48,10 @@ SIGNATURES = {
     "hpgStiffnessFactor": [_P, _P, _P, _P, _P, _P],
     "hpgStiffnessSolve": [_P, _P, _P, _P],
     "hpgSchurApply": [_P, _P, _D, _D, _P, _P, _P],
+    "hpgUFullSetup": [_P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "hpgUFullValues": [_P, _P, _P, _P],
+    "hpgUFullOperator": [_P, _D, _P, _P, _P, _P, _P],
+    "hpgUFullSolve": [_P, _P, _P, _P],
     "hpgVersion": [],
 }
 

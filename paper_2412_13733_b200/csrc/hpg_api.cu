@@ -15,6 +15,7 @@
 #include "hpg_launch.cuh"
 #include "hpg_precond.cuh"
 #include "hpg_schur.cuh"
+#include "hpg_qvi.cuh"
 
 #include <cublas_v2.h>
 #include "hpg_useside.cuh"
@@ -101,11 +102,26 @@ struct hpgPlan_st {
   int* cell_key = nullptr;       // [N]
   int nkeys = 0;
 
-  // fast-diagonalisation stiffness solve + Schur apply scratch
+  // fast-diagonalisation solves: interior stiffness A (fdm[0]) and the QVI
+  // full-space H = A_full + gamma M_full (fdm[1]); Schur apply scratch
   cublasHandle_t cub = nullptr;
-  double *Vx = nullptr, *Vy = nullptr, *finv = nullptr, *fw1 = nullptr, *fw2 = nullptr;
+  struct Fdm {
+    int r = 0, c = 0;
+    double *Vx = nullptr, *Vy = nullptr, *finv = nullptr, *w1 = nullptr, *w2 = nullptr;
+    bool ready = false;
+    void release() {
+      cudaFree(Vx); cudaFree(Vy); cudaFree(finv); cudaFree(w1); cudaFree(w2);
+      Vx = Vy = finv = w1 = w2 = nullptr;
+      ready = false;
+    }
+  } fdm[2];
   double *su1 = nullptr, *su2 = nullptr, *syD = nullptr, *sz = nullptr;
   bool fdm_ready = false;
+  // QVI full-space operator tables and scratch
+  double *qSR = nullptr, *qTR = nullptr, *qK = nullptr, *qM = nullptr;
+  double *qC = nullptr, *qT = nullptr, *qV = nullptr, *qG = nullptr, *qP1 = nullptr, *qP2 = nullptr;
+  double *qH1 = nullptr, *qH2 = nullptr, *qH3 = nullptr;
+  bool q_ready = false;
 
   int zcells = 0;
   int* dflag = nullptr;
@@ -295,8 +311,11 @@ int hpgPlanDestroy(hpgPlan P) {
   cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
   cudaFree(P->partial); cudaFree(P->Z); cudaFree(P->dflag); cudaFree(P->edge); cudaFree(P->PKG); cudaFree(P->ubuf);
   cudaFree(P->tri); cudaFree(P->cell_key);
-  cudaFree(P->Vx); cudaFree(P->Vy); cudaFree(P->finv); cudaFree(P->fw1); cudaFree(P->fw2);
+  P->fdm[0].release(); P->fdm[1].release();
   cudaFree(P->su1); cudaFree(P->su2); cudaFree(P->syD); cudaFree(P->sz);
+  cudaFree(P->qSR); cudaFree(P->qTR); cudaFree(P->qK); cudaFree(P->qM); cudaFree(P->qC); cudaFree(P->qT);
+  cudaFree(P->qV); cudaFree(P->qG); cudaFree(P->qP1); cudaFree(P->qP2); cudaFree(P->qH1); cudaFree(P->qH2);
+  cudaFree(P->qH3);
   if (P->cub) cublasDestroy(P->cub);
   delete P;
   return HPG_OK;
@@ -761,27 +780,35 @@ int hpgLUProfile(unsigned long long* counters) {
       return fail(HPG_ERR_CUDA, std::string(#x) + ": cublas status " + std::to_string((int)_st)); \
   } while (0)
 
+static int fdm_setup(hpgPlan P, int slot, int r, int c, const double* Vx, const double* lx, const double* Vy,
+                     const double* ly, double shift) {
+  if (P->cub == nullptr) CUBLAS_TRY(cublasCreate(&P->cub));
+  auto& F = P->fdm[slot];
+  F.release();
+  F.r = r; F.c = c;
+  std::vector<double> finv((size_t)r * c);
+  for (long long i = 0; i < r; ++i)
+    for (long long j = 0; j < c; ++j) finv[(size_t)(i * c + j)] = 1.0 / (lx[i] + ly[j] + shift);
+  int rc;
+  if ((rc = upload(&F.Vx, Vx, (size_t)r * r))) return rc;
+  if ((rc = upload(&F.Vy, Vy, (size_t)c * c))) return rc;
+  if ((rc = upload(&F.finv, finv.data(), finv.size()))) return rc;
+  CUDA_TRY(cudaMalloc(&F.w1, sizeof(double) * (size_t)r * c + 16));
+  CUDA_TRY(cudaMalloc(&F.w2, sizeof(double) * (size_t)r * c + 16));
+  F.ready = true;
+  return HPG_OK;
+}
+
 int hpgStiffnessFactor(hpgPlan P, const double* Vx, const double* lx, const double* Vy, const double* ly,
                        void* stream) {
   if (int rc = check(P)) return rc;
   if (!Vx || !lx || !Vy || !ly) return fail(HPG_ERR_ARG, "null eigen-factors");
-  const long long nix = P->nix, niy = P->niy;
-  if (nix <= 0 || niy <= 0) return fail(HPG_ERR_ARG, "mesh has no interior U dofs");
+  if (P->nix <= 0 || P->niy <= 0) return fail(HPG_ERR_ARG, "mesh has no interior U dofs");
   (void)stream;
-  if (P->cub == nullptr) CUBLAS_TRY(cublasCreate(&P->cub));
-  std::vector<double> finv((size_t)nix * niy);
-  for (long long i = 0; i < nix; ++i)
-    for (long long j = 0; j < niy; ++j) finv[(size_t)(i * niy + j)] = 1.0 / (lx[i] + ly[j]);
-  cudaFree(P->Vx); cudaFree(P->Vy); cudaFree(P->finv); cudaFree(P->fw1); cudaFree(P->fw2);
-  cudaFree(P->su1); cudaFree(P->su2); cudaFree(P->syD); cudaFree(P->sz);
-  P->Vx = P->Vy = P->finv = P->fw1 = P->fw2 = P->su1 = P->su2 = P->syD = P->sz = nullptr;
   P->fdm_ready = false;
-  int rc;
-  if ((rc = upload(&P->Vx, Vx, (size_t)(nix * nix)))) return rc;
-  if ((rc = upload(&P->Vy, Vy, (size_t)(niy * niy)))) return rc;
-  if ((rc = upload(&P->finv, finv.data(), finv.size()))) return rc;
-  CUDA_TRY(cudaMalloc(&P->fw1, sizeof(double) * nix * niy + 16));
-  CUDA_TRY(cudaMalloc(&P->fw2, sizeof(double) * nix * niy + 16));
+  cudaFree(P->su1); cudaFree(P->su2); cudaFree(P->syD); cudaFree(P->sz);
+  P->su1 = P->su2 = P->syD = P->sz = nullptr;
+  if (int rc = fdm_setup(P, 0, P->nix, P->niy, Vx, lx, Vy, ly, 0.0)) return rc;
   CUDA_TRY(cudaMalloc(&P->su1, sizeof(double) * P->ndof_u + 16));
   CUDA_TRY(cudaMalloc(&P->su2, sizeof(double) * P->ndof_u + 16));
   CUDA_TRY(cudaMalloc(&P->syD, sizeof(double) * P->ndof_psi + 16));
@@ -799,17 +826,32 @@ static int rm_gemm(hpgPlan P, bool ta, bool tb, int M, int N, int K, const doubl
   return HPG_OK;
 }
 
-static int stiffness_solve(hpgPlan P, const double* b, double* x, cudaStream_t s) {
-  const int nix = P->nix, niy = P->niy;
+// the same, batched with strides (stride 0 = shared operand)
+static int rm_gemm_batched(hpgPlan P, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
+                           long long sA, const double* B, int ldb, long long sB, double* C, int ldc, long long sC,
+                           int batch) {
+  const double one = 1.0, zero = 0.0;
+  CUBLAS_TRY(cublasDgemmStridedBatched(P->cub, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N,
+                                       M, K, &one, B, ldb, sB, A, lda, sA, &zero, C, ldc, sC, batch));
+  return HPG_OK;
+}
+
+static int fdm_solve(hpgPlan P, int slot, const double* b, double* x, cudaStream_t s) {
+  auto& F = P->fdm[slot];
+  const int r = F.r, c = F.c;
   CUBLAS_TRY(cublasSetStream(P->cub, s));
   int rc;
-  if ((rc = rm_gemm(P, true, false, nix, niy, nix, P->Vx, nix, b, niy, P->fw1, niy))) return rc;        // Vx^T B
-  if ((rc = rm_gemm(P, false, false, nix, niy, niy, P->fw1, niy, P->Vy, niy, P->fw2, niy))) return rc;  // . Vy
-  const long long n = (long long)nix * niy;
-  k_fdm_scale<<<(int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16), 256, 0, s>>>(P->fw2, P->finv, n);
+  if ((rc = rm_gemm(P, true, false, r, c, r, F.Vx, r, b, c, F.w1, c))) return rc;        // Vx^T B
+  if ((rc = rm_gemm(P, false, false, r, c, c, F.w1, c, F.Vy, c, F.w2, c))) return rc;    // . Vy
+  const long long n = (long long)r * c;
+  k_fdm_scale<<<(int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16), 256, 0, s>>>(F.w2, F.finv, n);
   LAUNCH_CHECK();
-  if ((rc = rm_gemm(P, false, false, nix, niy, nix, P->Vx, nix, P->fw2, niy, P->fw1, niy))) return rc;  // Vx .
-  return rm_gemm(P, false, true, nix, niy, niy, P->fw1, niy, P->Vy, niy, x, niy);                        // . Vy^T
+  if ((rc = rm_gemm(P, false, false, r, c, r, F.Vx, r, F.w2, c, F.w1, c))) return rc;    // Vx .
+  return rm_gemm(P, false, true, r, c, c, F.w1, c, F.Vy, c, x, c);                        // . Vy^T
+}
+
+static int stiffness_solve(hpgPlan P, const double* b, double* x, cudaStream_t s) {
+  return fdm_solve(P, 0, b, x, s);
 }
 
 int hpgStiffnessSolve(hpgPlan P, const double* b, double* x, void* stream) {
@@ -839,6 +881,121 @@ int hpgSchurApply(hpgPlan P, const double* wcache, double alpha, double beta, co
   k_schur_combine<<<grid, 256, 0, s>>>(A, P->kind == HPG_GRADIENT, alpha, beta, x, P->syD, P->sz, y);
   LAUNCH_CHECK();
   return HPG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// QVI temperature operators on the full U space (qvi.py:35-127)
+
+int hpgUFullSetup(hpgPlan P, double gamma, const double* SR, const double* TR, const double* Kh,
+                  const double* Mh, const double* Vx, const double* lx, const double* Vy, const double* ly,
+                  void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!SR || !TR || !Kh || !Mh || !Vx || !lx || !Vy || !ly) return fail(HPG_ERR_ARG, "null table");
+  if (P->p < 2) return fail(HPG_ERR_UNSUPPORTED, "full-space U operators need p >= 2");
+  (void)stream;
+  const int m = P->m, Q = P->nq, N = P->N;
+  const int nfx = P->ncx * P->p + 1, nfy = P->ncy * P->p + 1;
+  P->q_ready = false;
+  double** bufs[] = {&P->qSR, &P->qTR, &P->qK, &P->qM, &P->qC, &P->qT, &P->qV, &P->qG,
+                     &P->qP1, &P->qP2, &P->qH1, &P->qH2, &P->qH3};
+  for (double** b : bufs) { cudaFree(*b); *b = nullptr; }
+  int rc;
+  if ((rc = upload(&P->qSR, SR, (size_t)Q * m))) return rc;
+  if ((rc = upload(&P->qTR, TR, (size_t)m * Q))) return rc;
+  if ((rc = upload(&P->qK, Kh, (size_t)m * m))) return rc;
+  if ((rc = upload(&P->qM, Mh, (size_t)m * m))) return rc;
+  const size_t mm = (size_t)N * m * m, qm = (size_t)N * Q * (Q > m ? Q : m), qq = (size_t)N * Q * Q;
+  CUDA_TRY(cudaMalloc(&P->qC, sizeof(double) * mm + 16));
+  CUDA_TRY(cudaMalloc(&P->qT, sizeof(double) * qm + 16));
+  CUDA_TRY(cudaMalloc(&P->qV, sizeof(double) * qq + 16));
+  CUDA_TRY(cudaMalloc(&P->qG, sizeof(double) * mm + 16));
+  CUDA_TRY(cudaMalloc(&P->qP1, sizeof(double) * mm + 16));
+  CUDA_TRY(cudaMalloc(&P->qP2, sizeof(double) * mm + 16));
+  CUDA_TRY(cudaMalloc(&P->qH1, sizeof(double) * mm + 16));
+  CUDA_TRY(cudaMalloc(&P->qH2, sizeof(double) * mm + 16));
+  CUDA_TRY(cudaMalloc(&P->qH3, sizeof(double) * mm + 16));
+  if ((rc = fdm_setup(P, 1, nfx, nfy, Vx, lx, Vy, ly, gamma))) return rc;
+  P->q_ready = true;
+  return HPG_OK;
+}
+
+static QArgs qargs(hpgPlan P) {
+  QArgs Q;
+  Q.ncx = P->ncx; Q.ncy = P->ncy; Q.p = P->p; Q.m = P->m; Q.nq = P->nq; Q.N = P->N;
+  Q.nfy = (long long)P->ncy * P->p + 1;
+  Q.hx = P->hx; Q.hy = P->hy;
+  return Q;
+}
+
+static int grid_for(long long n) { long long g = (n + 255) / 256; return (int)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16); }
+
+// V = SR C SR^T for the full vector v (into P->qV); C kept in P->qC
+static int q_values(hpgPlan P, const double* v, cudaStream_t s) {
+  const int m = P->m, Q = P->nq, N = P->N;
+  QArgs A = qargs(P);
+  k_qgather<<<grid_for((long long)N * m * m), 256, 0, s>>>(A, v, P->qC);
+  LAUNCH_CHECK();
+  CUBLAS_TRY(cublasSetStream(P->cub, s));
+  int rc;
+  if ((rc = rm_gemm_batched(P, false, false, Q, m, m, P->qSR, m, 0, P->qC, m, (long long)m * m, P->qT, m,
+                            (long long)Q * m, N)))
+    return rc;
+  return rm_gemm_batched(P, false, true, Q, Q, m, P->qT, m, (long long)Q * m, P->qSR, m, 0, P->qV, Q,
+                         (long long)Q * Q, N);
+}
+
+int hpgUFullValues(hpgPlan P, const double* v, double* vals, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!P->q_ready) return fail(HPG_ERR_ARG, "hpgUFullSetup has not been called on this plan");
+  if (!v || !vals) return fail(HPG_ERR_ARG, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = q_values(P, v, s)) return rc;
+  CUDA_TRY(cudaMemcpyAsync(vals, P->qV, sizeof(double) * (size_t)P->N * P->nq * P->nq, cudaMemcpyDeviceToDevice, s));
+  return HPG_OK;
+}
+
+int hpgUFullOperator(hpgPlan P, double gamma, const double* v, const double* w, const double* rhs, double* out,
+                     void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!P->q_ready) return fail(HPG_ERR_ARG, "hpgUFullSetup has not been called on this plan");
+  if (!out) return fail(HPG_ERR_ARG, "null pointer");
+  if (w && !v) return fail(HPG_ERR_ARG, "weights given without a vector");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int m = P->m, Q = P->nq, N = P->N;
+  const long long mm = (long long)m * m, qq = (long long)Q * Q;
+  CUBLAS_TRY(cublasSetStream(P->cub, s));
+  int rc;
+  if (v) {
+    if ((rc = q_values(P, v, s))) return rc;                 // C = tiles(v), V = values(v)
+    // H terms: Kh C Mh, Mh C Kh, Mh C Mh
+    if ((rc = rm_gemm_batched(P, false, false, m, m, m, P->qK, m, 0, P->qC, m, mm, P->qP1, m, mm, N))) return rc;
+    if ((rc = rm_gemm_batched(P, false, false, m, m, m, P->qM, m, 0, P->qC, m, mm, P->qP2, m, mm, N))) return rc;
+    if ((rc = rm_gemm_batched(P, false, true, m, m, m, P->qP1, m, mm, P->qM, m, 0, P->qH1, m, mm, N))) return rc;
+    if ((rc = rm_gemm_batched(P, false, true, m, m, m, P->qP2, m, mm, P->qK, m, 0, P->qH2, m, mm, N))) return rc;
+    if ((rc = rm_gemm_batched(P, false, true, m, m, m, P->qP2, m, mm, P->qM, m, 0, P->qH3, m, mm, N))) return rc;
+  }
+  const bool load = w || rhs;
+  if (load) {
+    k_qpoint<<<grid_for((long long)N * qq), 256, 0, s>>>((long long)N * qq, P->qV, w, rhs);
+    LAUNCH_CHECK();
+    if ((rc = rm_gemm_batched(P, false, false, m, Q, Q, P->qTR, Q, 0, P->qV, Q, qq, P->qT, Q, (long long)m * Q, N)))
+      return rc;
+    if ((rc = rm_gemm_batched(P, false, true, m, m, Q, P->qT, Q, (long long)m * Q, P->qTR, Q, 0, P->qG, m, mm, N)))
+      return rc;
+  }
+  QArgs A = qargs(P);
+  const long long nfull = ((long long)P->ncx * P->p + 1) * A.nfy;
+  k_qscatter<<<grid_for(nfull), 256, 0, s>>>(A, gamma, v ? P->qH1 : nullptr, v ? P->qH2 : nullptr,
+                                             v ? P->qH3 : nullptr, load ? P->qG : nullptr, out);
+  LAUNCH_CHECK();
+  return HPG_OK;
+}
+
+int hpgUFullSolve(hpgPlan P, const double* b, double* x, void* stream) {
+  if (int rc = check(P)) return rc;
+  if (!P->q_ready) return fail(HPG_ERR_ARG, "hpgUFullSetup has not been called on this plan");
+  if (!b || !x || b == x) return fail(HPG_ERR_ARG, "bad pointers");
+  return fdm_solve(P, 1, b, x, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -40,3 +40,18 @@ def load_solve(name):
     d["line_search"] = bool(d["line_search"])
     d["converged"] = bool(d["converged"])
     return d
+
+
+def qvi_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "qvi", "*.npz")))
+
+
+def load_qvi(name):
+    with np.load(os.path.join(GOLDEN, "qvi", name + ".npz"), allow_pickle=False) as z:
+        d = {k: z[k] for k in z.files}
+    d["rule"] = str(d["rule"])
+    for k in ("p", "nq", "newton"):
+        d[k] = int(d[k])
+    for k in ("load", "gamma"):
+        d[k] = float(d[k])
+    return d
