@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhpg_b200.so")
+LIB_PATH = os.environ.get("HPG_LIB") or os.path.join(_HERE, "libhpg_b200.so")   # HPG_LIB: A/B experiments
 
 HPG_OBSTACLE = 0
 HPG_GRADIENT = 1

@@ -407,6 +407,13 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
   } else {
     A.phi = phi; A.flag = P->dflag;
   }
+  if (P->kind == HPG_OBSTACLE && P->small && wcache == nullptr && lowp_available(P->p, P->nq) &&
+      getenv("HPG_LOWP_OFF") == nullptr) {
+    // low degree: the whole residual (+ Jacobian apply at the same psi) in one
+    // single-pass kernel (hpg_lowp.cu)
+    if (x != nullptr) { A.in1 = x; A.wc_out = y; }
+    return run_lowp(P->p, P->nq, x != nullptr, A, P->stab, s);
+  }
   if (usmall_available(P->p, P->kind == HPG_GRADIENT)) {
     // (1) U side, low degree: thread per cell, generated straight-line code
     if ((rc = run_usmall(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;

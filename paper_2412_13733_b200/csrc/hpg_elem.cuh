@@ -122,45 +122,144 @@ __device__ __forceinline__ void map_pair(const ElemArgs& A, int e, int QT, int r
   }
 }
 
+// Stage (b) of the cached modes with the weights already in registers
+// (C-fragment pair j = 0, 1 of tile (rt, ht); padded points carry weight 0).
+template <int MODE, int NSYN, int NOUT, int NW>
+__device__ __forceinline__ void map_pair_w(const double (&V)[NSYN > 0 ? NSYN : 1][2],
+                                           const double (&W)[NW > 0 ? NW : 1][2],
+                                           double (&Vw)[NOUT][2], bool row_in, int h0, int nq) {
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool inside = row_in && h0 + j < nq;
+    double v[NSYN > 0 ? NSYN : 1], wi[NW > 0 ? NW : 1], wo[NW > 0 ? NW : 1], vw[NOUT];
+#pragma unroll
+    for (int f = 0; f < NSYN; ++f) v[f] = V[f][j];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) wi[w] = W[w][j];
+    bool fl = false;
+    point_map<MODE>(v, 0.0, wi, wo, vw, fl);
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) Vw[o][j] = inside ? vw[o] : 0.0;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Warp-per-element kernel: all fragments in registers, tables in smem.
+//
+// Latency structure (one wave: the grid never exceeds the resident slots):
+//  * launched with programmatic stream serialization (PDL): the table fill
+//    into shared memory runs while the previous kernel drains, then
+//    griddepcontrol.wait orders every read of psi / x / weights after it;
+//  * small tiles (NIN*2*NT^2 <= 8 doubles) skip the shared-memory staging:
+//    each lane loads exactly the B-fragment entries C[8(ks>>1)+2c+(ks&1)][8nt+r]
+//    it feeds to the first contraction (rows of 8 consecutive doubles);
+//  * cached modes prefetch the next row tile's point weights one iteration
+//    ahead, so the map never waits on L2.
 template <int NT, int QT, int MODE>
-__global__ void __launch_bounds__(32 * WARP_CTA_WARPS)
+struct WarpCfg {
+  using TR = ModeTraits<MODE>;
+  static constexpr bool REGX = TR::NIN * 2 * NT * NT <= (MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED ? 8 : 4);
+  static constexpr bool cached = MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED;
+  // cached modes: the cell's point weights are copied to shared memory with
+  // cp.async when they fit (<= 16 KB per warp), read back by the same lane
+  static constexpr int WDBL = QT * QT * TR::NW * 64;
+  static constexpr bool WSMEM = cached && WDBL * 8 <= 16 * 1024;
+  // 4096 cells (config 1) must fit one wave of 4-warp CTAs: >= 7 CTAs / SM
+  static constexpr int MINB = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? 7 : 1;
+};
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int NT, int QT, int MODE>
+__global__ void __launch_bounds__(32 * WARP_CTA_WARPS, (WarpCfg<NT, QT, MODE>::MINB))
 k_warp(ElemArgs A) {
   using TR = ModeTraits<MODE>;
+  using CF = WarpCfg<NT, QT, MODE>;
   constexpr int NP = 8 * NT, QP = 8 * QT, NK = NP / 4, QK = QP / 4;
   constexpr int LDT = NP + 2, TILE = NP * LDT;
   constexpr int NIN = TR::NIN, NSYN = TR::NSYN, NOUT = TR::NOUT, NW = TR::NW;
+  constexpr bool REGX = CF::REGX, cached = CF::cached, WSMEM = CF::WSMEM;
+  constexpr int NSTAGE = REGX ? 0 : NIN;
+  constexpr int WDBL = WSMEM ? CF::WDBL : 0;
   extern __shared__ double smem[];
   double* sS = smem;
   double* sT = sS + QP * NP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
-  double* sTile = sT + NP * QP + warp * (NIN > 0 ? NIN * TILE : 0);
-  double* sInv = sT + NP * QP + WARP_CTA_WARPS * NIN * TILE;      // 1/(2k+1), k < NP
-  for (int i = threadIdx.x; i < QP * NP; i += blockDim.x) {
-    sS[i] = A.Sf[i];
-    sT[i] = A.Tf[i];
+  double* sTile = sT + NP * QP + warp * (NSTAGE > 0 ? NSTAGE * TILE : 0);
+  double* sW = sT + NP * QP + WARP_CTA_WARPS * NSTAGE * TILE + warp * WDBL;   // [rt][ht][w][lane][2]
+  double* sInv = sT + NP * QP + WARP_CTA_WARPS * (NSTAGE * TILE + WDBL);      // 1/(2k+1), k < NP
+  // tables: every copy in flight at once (cp.async, no register staging)
+  for (int i = 2 * threadIdx.x; i < QP * NP; i += 2 * blockDim.x) {
+    cp_async16(sS + i, A.Sf + i);
+    cp_async16(sT + i, A.Tf + i);
   }
+  cp_async_commit();
   for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
-  __syncthreads();
+  // one wave: let the next kernel in the stream stage its tables now
+  pdl_trigger();
+  pdl_wait();
 
-  for (int e = blockIdx.x * WARP_CTA_WARPS + warp; e < A.N; e += gridDim.x * WARP_CTA_WARPS) {
+  double X[REGX ? NIN : 1][REGX ? NK : 1][REGX ? NT : 1];
+  // issue the loads of cell e: the first contraction's B fragments (registers
+  // or the warp's staging tile) and the row-tile-0 weights of cached modes
+  auto load_cell = [&](int e) {
     const int cx = e / A.ncy, cy = e - cx * A.ncy;
+    if constexpr (REGX) {
 #pragma unroll
-    for (int f = 0; f < NIN; ++f) {
-      const double* src;
-      int comp;
-      field_src<MODE>(A, f, src, comp);
-      src += comp * A.ncomp;
-      for (int idx = lane; idx < NP * NP; idx += 32) {
-        int a = idx / NP, b = idx - a * NP;
-        double v = 0.0;
-        if (a < A.n && b < A.n) v = __ldg(src + psi_index(A, cx, cy, a, b));
-        sTile[f * TILE + a * LDT + b] = v;
+      for (int f = 0; f < NIN; ++f) {
+        const double* src;
+        int comp;
+        field_src<MODE>(A, f, src, comp);
+        src += comp * A.ncomp + psi_index(A, cx, cy, 0, 0);
+#pragma unroll
+        for (int ks = 0; ks < NK; ++ks) {
+          const int a = 8 * (ks >> 1) + 2 * c + (ks & 1);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int b = 8 * nt + r;
+            X[f][ks][nt] = (a < A.n && b < A.n) ? __ldg(src + (long long)a * A.ld + b) : 0.0;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < NIN; ++f) {
+        const double* src;
+        int comp;
+        field_src<MODE>(A, f, src, comp);
+        src += comp * A.ncomp;
+        for (int idx = lane; idx < NP * NP; idx += 32) {
+          int a = idx / NP, b = idx - a * NP;
+          double v = 0.0;
+          if (a < A.n && b < A.n) v = __ldg(src + psi_index(A, cx, cy, a, b));
+          sTile[f * TILE + a * LDT + b] = v;
+        }
       }
     }
-    __syncwarp();
+    if constexpr (WSMEM) {
+      const double* src = A.wc_in + wc_index(e, QT, 0, 0, NW, 0, lane);
+#pragma unroll
+      for (int t = 0; t < QT * QT * NW; ++t) cp_async16(sW + t * 64 + 2 * lane, src + t * 64);
+      cp_async_commit();
+    }
+  };
+  const int stride = gridDim.x * WARP_CTA_WARPS;
+  int e = blockIdx.x * WARP_CTA_WARPS + warp;
+  if (e < A.N) load_cell(e);
+  cp_async_wait_all();
+  __syncthreads();   // tables
+
+  for (; e < A.N; e += stride) {
+    const int cx = e / A.ncy, cy = e - cx * A.ncy;
+    if constexpr (!REGX) __syncwarp();
     double Y[NOUT][NT][NT][2];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
@@ -181,9 +280,14 @@ k_warp(ElemArgs A) {
 #pragma unroll
         for (int ks = 0; ks < NK; ++ks) {
           double a = sS[(rt * NK + ks) * 32 + lane];
-          const double* row = sTile + f * TILE + (8 * (ks >> 1) + 2 * c + (ks & 1)) * LDT + r;
+          if constexpr (REGX) {
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma(P[nt], a, row[8 * nt]);
+            for (int nt = 0; nt < NT; ++nt) dmma(P[nt], a, X[f][ks][nt]);
+          } else {
+            const double* row = sTile + f * TILE + (8 * (ks >> 1) + 2 * c + (ks & 1)) * LDT + r;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(P[nt], a, row[8 * nt]);
+          }
         }
 #pragma unroll
         for (int ht = 0; ht < QT; ++ht) {
@@ -200,7 +304,19 @@ k_warp(ElemArgs A) {
 #pragma unroll
         for (int f = 0; f < NSYN; ++f) { Vp[f][0] = V[f][ht][0]; Vp[f][1] = V[f][ht][1]; }
         double out2[NOUT][2];
-        map_pair<MODE, NSYN, NOUT, NW>(A, e, QT, rt, ht, lane, Vp, out2, flag);
+        if constexpr (WSMEM) {
+          if (rt == 0 && ht == 0) cp_async_wait_all();
+          double Wc[NW][2];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const double2 t = *reinterpret_cast<const double2*>(sW + ((rt * QT + ht) * NW + w) * 64 + 2 * lane);
+            Wc[w][0] = t.x;
+            Wc[w][1] = t.y;
+          }
+          map_pair_w<MODE, NSYN, NOUT, NW>(Vp, Wc, out2, 8 * rt + r < A.nq, 8 * ht + 2 * c, A.nq);
+        } else {
+          map_pair<MODE, NSYN, NOUT, NW>(A, e, QT, rt, ht, lane, Vp, out2, flag);
+        }
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) { Vw[o][ht][0] = out2[o][0]; Vw[o][ht][1] = out2[o][1]; }
       }
@@ -226,6 +342,10 @@ k_warp(ElemArgs A) {
     if constexpr (MODE == M_OBST_RES) {
       if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
     }
+    // REGX / cp.async: the next cell's loads are in flight during the epilogue
+    if constexpr (REGX) {
+      if (e + stride < A.N) load_cell(e + stride);
+    }
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
 #pragma unroll
@@ -237,7 +357,10 @@ k_warp(ElemArgs A) {
             int a = 8 * at + 2 * c + j, b = 8 * bt + r;
             if (a < A.n && b < A.n) write_moment<MODE>(A, e, cx, cy, o, a, b, Y[o][bt][at][j], sInv);
           }
-    __syncwarp();
+    if constexpr (!REGX) {
+      __syncwarp();
+      if (e + stride < A.N) load_cell(e + stride);
+    }
   }
 }
 

@@ -25,6 +25,10 @@ int run_small(int n, int q, bool res, bool apply, const ElemArgs& A, const Small
 bool usmall_available(int p, bool gradient);
 int run_usmall(int p, bool gradient, const ElemArgs& A, cudaStream_t s);
 
+// Single-pass residual (+ apply) for low-degree obstacle meshes (hpg_lowp.cu).
+bool lowp_available(int p, int q);
+int run_lowp(int p, int q, bool apply, const ElemArgs& A, const SmallTables& tb, cudaStream_t s);
+
 // Warp-per-cell generated-pass U side for mid degrees (hpg_upass.cu).
 bool upass_available(int p);
 int run_upass(int p, bool gradient, const ElemArgs& A, cudaStream_t s);

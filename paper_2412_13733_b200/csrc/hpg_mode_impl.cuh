@@ -1,6 +1,7 @@
 // Instantiation body shared by the hpg_mode_*.cu translation units.
 // Define HPG_MODE and the warp (NT, QT) list (HPG_WARP_LIST) before including.
 #pragma once
+#include <cstdlib>
 #include "hpg_elem.cuh"
 #include "hpg_launch.cuh"
 
@@ -11,7 +12,9 @@ template <int NT, int QT, int MODE>
 int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
   constexpr int NP = 8 * NT, QP = 8 * QT;
-  const size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * TR::NIN * NP * (NP + 2) + NP +
+  constexpr int NSTAGE = WarpCfg<NT, QT, MODE>::REGX ? 0 : TR::NIN;
+  constexpr int WDBL = WarpCfg<NT, QT, MODE>::WSMEM ? WarpCfg<NT, QT, MODE>::WDBL : 0;
+  const size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * (NSTAGE * NP * (NP + 2) + WDBL) + NP +
                                         (size_t)WARP_CTA_WARPS * A.usmem);
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "warp path shared memory too large");
   static size_t attr = 0;
@@ -32,8 +35,21 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   }
   int need = (A.N + WARP_CTA_WARPS - 1) / WARP_CTA_WARPS;
   int grid = need < nsm * occ ? need : nsm * occ;
-  k_warp<NT, QT, MODE><<<grid, 32 * WARP_CTA_WARPS, smem, s>>>(A);
-  cudaError_t e = cudaGetLastError();
+  // programmatic dependent launch: the table prologue overlaps the previous
+  // kernel's tail (k_warp orders its data reads with griddepcontrol.wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32 * WARP_CTA_WARPS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  static const bool pdl = getenv("HPG_NO_PDL") == nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_warp<NT, QT, MODE>, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_warp launch", e);
 }
 

@@ -12,7 +12,9 @@ FMA sequences with literal reference-cell coefficients:
 
 R: U dof -> Legendre map (spaces.py:45-57), D: derivative map (:59-68),
 Kref = h * local stiffness, Mref = R^T diag(1/(2l+1)) R = local mass / h.
-Coefficients are exact rationals evaluated in fp64 here.
+Coefficients are exact rationals evaluated in fp64 here.  C and G are any
+indexable operands (shared-memory slices in k_usmall, lazy global-memory
+accessors in k_lowp, where dead outputs and their loads are eliminated).
 
     python tools/gen_usmall.py        (rewrites the header)
 """
@@ -70,9 +72,9 @@ def gen(p, gradient):
     lines = []
     w = lines.append
     w(f"template <> struct USmall<{p}, {'true' if gradient else 'false'}> {{")
-    w("template <class OU, class OB>")
+    w("template <class CA, class GA, class OU, class OB>")
     w("__device__ __forceinline__ static void run(")
-    w("    const double* __restrict__ C, const double* __restrict__ G, int TH, double hx, double hy,")
+    w("    const CA& C, const GA& G, int TH, double hx, double hy,")
     w("    double alpha, OU ou, OB ob) {")
     w(f"  // p = {p}: m = {m}, n = {n}; C[(i*{m}+l)*TH], G[((comp*{n}+i)*{n}+l)*TH] (raw psi_prev - psi)")
     w("  const double sKM = hy / hx, sMK = hx / hy;")
