@@ -166,6 +166,10 @@ struct WarpCfg {
   static constexpr bool WSMEM = cached && WDBL * 8 <= 16 * 1024;
   // 4096 cells (config 1) must fit one wave of 4-warp CTAs: >= 7 CTAs / SM
   static constexpr int MINB = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? 7 : 1;
+#ifndef HPG_UNROLL_RT
+#define HPG_UNROLL_RT 0
+#endif
+  static constexpr bool UNROLL_RT = HPG_UNROLL_RT && cached && QT <= 3;
 };
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
@@ -185,7 +189,7 @@ k_warp(ElemArgs A) {
   constexpr int NP = 8 * NT, QP = 8 * QT, NK = NP / 4, QK = QP / 4;
   constexpr int LDT = NP + 2, TILE = NP * LDT;
   constexpr int NIN = TR::NIN, NSYN = TR::NSYN, NOUT = TR::NOUT, NW = TR::NW;
-  constexpr bool REGX = CF::REGX, cached = CF::cached, WSMEM = CF::WSMEM;
+  constexpr bool REGX = CF::REGX, WSMEM = CF::WSMEM;
   constexpr int NSTAGE = REGX ? 0 : NIN;
   constexpr int WDBL = WSMEM ? CF::WDBL : 0;
   extern __shared__ double smem[];
@@ -269,7 +273,9 @@ k_warp(ElemArgs A) {
         for (int k = 0; k < NT; ++k) Y[o][i][k][0] = Y[o][i][k][1] = 0.0;
     bool flag = false;
 
-#pragma unroll 1
+    // cached small tiles: unrolled row-tile loop, so the scheduler can overlap
+    // the synthesis of row tile rt+1 with the analysis of rt
+#pragma unroll (CF::UNROLL_RT ? QT : 1)
     for (int rt = 0; rt < QT; ++rt) {
       double V[NSYN > 0 ? NSYN : 1][QT][2];
 #pragma unroll

@@ -58,10 +58,33 @@ struct GLazy {
 
 constexpr int LOWP_TH = 64;
 
+// operand read through a callable (register arrays with constant indices)
+template <class F>
+struct FnAcc {
+  F f;
+  __device__ __forceinline__ double operator[](int k) const { return f(k); }
+};
+template <class F>
+__device__ __forceinline__ FnAcc<F> fn_acc(F f) { return FnAcc<F>{f}; }
+
+// thread-private shared-memory slice: T[k] = s[k * LOWP_TH]
+struct Slice {
+  const double* s;
+  __device__ __forceinline__ double operator[](int k) const { return s[k * LOWP_TH]; }
+};
+
 template <int P, int Q, bool APPLY>
-__global__ void __launch_bounds__(LOWP_TH) k_lowp(ElemArgs A, const SmallTables tb) {
+// p <= 4: <= 146 registers keeps the 65,536-cell mesh in one wave; p >= 5
+// runs unconstrained (capping it spills the U-side operands: measured slower)
+#ifndef HPG_LOWP_MINB_SMALL
+#define HPG_LOWP_MINB_SMALL 7
+#endif
+__global__ void __launch_bounds__(LOWP_TH, P <= 4 ? HPG_LOWP_MINB_SMALL : 1) k_lowp(ElemArgs A, const SmallTables tb) {
   constexpr int N = P - 1, M = P + 1, NIN = APPLY ? 2 : 1;
-  __shared__ double sC[NIN][N * N][LOWP_TH];     // thread-private tile slices
+  constexpr int SL = NIN * N * N > M * M ? NIN * N * N : M * M;
+  // thread-private slices: psi (and x) tiles in (1), then the U tile in (2)
+  __shared__ double sbuf[SL][LOWP_TH];
+  double (*sC)[N * N][LOWP_TH] = reinterpret_cast<double (*)[N * N][LOWP_TH]>(&sbuf[0][0]);
   const int tid = threadIdx.x;
   const int e = blockIdx.x * LOWP_TH + tid;
   if (e >= A.N) return;
@@ -75,6 +98,23 @@ __global__ void __launch_bounds__(LOWP_TH) k_lowp(ElemArgs A, const SmallTables 
       sC[0][a * N + b][tid] = __ldg(A.in0 + base + (long long)a * A.ld + b);
       if (APPLY) sC[NIN - 1][a * N + b][tid] = __ldg(A.in1 + base + (long long)a * A.ld + b);
     }
+  // low degree: the U-side operands are loaded now, so their latency hides
+  // behind the psi-side arithmetic (the kernel is otherwise a chain of
+  // dependent round trips at p <= 4)
+  constexpr bool PREF = P <= 3;
+  double uC[PREF ? M * M : 1], pp[PREF ? N * N : 1], ph[PREF ? N * N : 1];
+  if constexpr (PREF) {
+    const ULazy<P> Cl{A.u, cx, cy, A.ncx, A.ncy, A.niy};
+#pragma unroll
+    for (int k = 0; k < M * M; ++k) uC[k] = Cl[k];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        pp[a * N + b] = __ldg(A.psi_prev + base + (long long)a * A.ld + b);
+        ph[a * N + b] = __ldg(A.phi_mom + base + (long long)a * A.ld + b);
+      }
+  }
   double Mm[N][N];
   double MY[APPLY ? N : 1][APPLY ? N : 1];
 #pragma unroll
@@ -149,8 +189,6 @@ __global__ void __launch_bounds__(LOWP_TH) k_lowp(ElemArgs A, const SmallTables 
 #pragma unroll
   for (int k = 0; k < M; ++k) H0k[k] = Hj0[k] = 0.0;
   {
-    const ULazy<P> Cu{A.u, cx, cy, A.ncx, A.ncy, A.niy};
-    const GLazy<N> Gp{A.psi_prev, A.in0, base, A.ld};
     auto ou = [&](int j, int k, double r) {
       if (j >= 2 && k >= 2) {
         const long long g = (bx + j) * A.niy + (by + k);
@@ -167,9 +205,27 @@ __global__ void __launch_bounds__(LOWP_TH) k_lowp(ElemArgs A, const SmallTables 
     auto ob = [&](int, int a, int b, double btu) {
       const long long g = base + (long long)a * A.ld + b;
       const double val = ((hx * kInvOdd[a]) * Mm[a][b]) * (hy * kInvOdd[b]);
-      A.out[g] = (__ldg(A.phi_mom + g) - btu) - val;
+      double phm;
+      if constexpr (PREF) phm = ph[a * N + b];
+      else phm = __ldg(A.phi_mom + g);
+      A.out[g] = (phm - btu) - val;
     };
-    USmall<P, false>::run(Cu, Gp, 1, hx, hy, alpha, ou, ob);
+    if constexpr (PREF) {
+      const auto Cu = fn_acc([&](int k) { return uC[k]; });
+      const auto Gp = fn_acc([&](int k) { return pp[k] - sC[0][k][tid]; });
+      USmall<P, false>::run(Cu, Gp, 1, hx, hy, alpha, ou, ob);
+    } else {
+      // the own U tile is used by every output: stage it once in this
+      // thread's slice (the psi-side tiles are dead); psi_prev - psi lazily
+      {
+        const ULazy<P> Cl{A.u, cx, cy, A.ncx, A.ncy, A.niy};
+#pragma unroll
+        for (int k = 0; k < M * M; ++k) sbuf[k][tid] = Cl[k];
+      }
+      const Slice Cu{&sbuf[0][tid]};
+      const GLazy<N> Gp{A.psi_prev, A.in0, base, A.ld};
+      USmall<P, false>::run(Cu, Gp, 1, hx, hy, alpha, ou, ob);
+    }
   }
   // ---- (3) neighbours' contributions to the owned hats -------------------
   auto nob = [](int, int, int, double) {};
