@@ -164,6 +164,7 @@ struct WarpCfg {
   // cp.async when they fit (<= 16 KB per warp), read back by the same lane
   static constexpr int WDBL = QT * QT * TR::NW * 64;
   static constexpr bool WSMEM = cached && WDBL * 8 <= 16 * 1024;
+  static constexpr bool WRITES_WC = MODE == M_OBST_RES || MODE == M_GRAD_RES;
   // 4096 cells (config 1) must fit one wave of 4-warp CTAs: >= 7 CTAs / SM
   static constexpr int MINB = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? 7 : 1;
 #ifndef HPG_UNROLL_RT
@@ -207,13 +208,29 @@ k_warp(ElemArgs A) {
   }
   cp_async_commit();
   for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
-  // one wave: let the next kernel in the stream stage its tables now
-  pdl_trigger();
+  // cached modes: the point weights of the first cell are copied BEFORE the
+  // grid-dependency wait.  This is safe because no PDL kernel that writes a
+  // weight cache triggers its dependents early (the residual modes below), so
+  // a weight cache is always complete when a kernel reading it is launched.
+  auto load_weights = [&](int e) {
+    if constexpr (WSMEM) {
+      const double* src = A.wc_in + wc_index(e, QT, 0, 0, NW, 0, lane);
+#pragma unroll
+      for (int t = 0; t < QT * QT * NW; ++t) cp_async16(sW + t * 64 + 2 * lane, src + t * 64);
+      cp_async_commit();
+    }
+  };
+  const int stride = gridDim.x * WARP_CTA_WARPS;
+  int e = blockIdx.x * WARP_CTA_WARPS + warp;
+  if (e < A.N) load_weights(e);
+  // one wave: let the next kernel in the stream start its prologue now --
+  // except kernels that write a weight cache (see load_weights)
+  if constexpr (!CF::WRITES_WC) pdl_trigger();
   pdl_wait();
 
   double X[REGX ? NIN : 1][REGX ? NK : 1][REGX ? NT : 1];
   // issue the loads of cell e: the first contraction's B fragments (registers
-  // or the warp's staging tile) and the row-tile-0 weights of cached modes
+  // or the warp's staging tile)
   auto load_cell = [&](int e) {
     const int cx = e / A.ncy, cy = e - cx * A.ncy;
     if constexpr (REGX) {
@@ -248,15 +265,7 @@ k_warp(ElemArgs A) {
         }
       }
     }
-    if constexpr (WSMEM) {
-      const double* src = A.wc_in + wc_index(e, QT, 0, 0, NW, 0, lane);
-#pragma unroll
-      for (int t = 0; t < QT * QT * NW; ++t) cp_async16(sW + t * 64 + 2 * lane, src + t * 64);
-      cp_async_commit();
-    }
   };
-  const int stride = gridDim.x * WARP_CTA_WARPS;
-  int e = blockIdx.x * WARP_CTA_WARPS + warp;
   if (e < A.N) load_cell(e);
   cp_async_wait_all();
   __syncthreads();   // tables
@@ -349,6 +358,7 @@ k_warp(ElemArgs A) {
       if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
     }
     // REGX / cp.async: the next cell's loads are in flight during the epilogue
+    if (e + stride < A.N) load_weights(e + stride);
     if constexpr (REGX) {
       if (e + stride < A.N) load_cell(e + stride);
     }
