@@ -433,8 +433,16 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     void* fn = P->kind == HPG_GRADIENT ? (void*)k_uside_pt<true> : (void*)k_uside_pt<false>;
     if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ElemArgs U = A;
-    void* args[] = {&U, &cpb, &TG};
-    CUDA_TRY(cudaLaunchKernel(fn, dim3((P->N + cpb - 1) / cpb), dim3(cpb * TG), args, smem, s));
+    // few large cells: split each cell's entries over several CTAs (one wave)
+    int usplit = 1;
+    if (cpb == 1 && P->N < P->nsm) {
+      const int blocks = (P->m * P->m + TG - 1) / TG;
+      usplit = P->nsm / P->N;
+      if (usplit > blocks) usplit = blocks;
+      if (usplit < 1) usplit = 1;
+    }
+    void* args[] = {&U, &cpb, &TG, &usplit};
+    CUDA_TRY(cudaLaunchKernel(fn, dim3((P->N + cpb - 1) / cpb * usplit), dim3(cpb * TG), args, smem, s));
     CUDA_TRY(cudaGetLastError());
   }
   // (2) psi side finishes b_psi in place (proximal.py:123 order)

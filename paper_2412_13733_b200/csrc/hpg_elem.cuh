@@ -165,8 +165,17 @@ struct WarpCfg {
   static constexpr int WDBL = QT * QT * TR::NW * 64;
   static constexpr bool WSMEM = cached && WDBL * 8 <= 16 * 1024;
   static constexpr bool WRITES_WC = MODE == M_OBST_RES || MODE == M_GRAD_RES;
+  // cached small tiles (config 1): 2-warp CTAs, each warp streams CPW = 2
+  // cells with the next cell's x fragments and weights in flight during the
+  // current cell's contractions (the load burst at kernel start is halved)
+#ifndef HPG_PIPE2
+#define HPG_PIPE2 0
+#endif
+  static constexpr bool PIPE = HPG_PIPE2 && cached && REGX && WSMEM && NT <= 2 && QT <= 3;
+  static constexpr int W = PIPE ? 2 : WARP_CTA_WARPS;
+  static constexpr int CPW = PIPE ? 2 : 1;
   // 4096 cells (config 1) must fit one wave of 4-warp CTAs: >= 7 CTAs / SM
-  static constexpr int MINB = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? 7 : 1;
+  static constexpr int MINB_ = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? 7 : 1;
 #ifndef HPG_UNROLL_RT
 #define HPG_UNROLL_RT 0
 #endif
@@ -181,9 +190,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
 
 template <int NT, int QT, int MODE>
-__global__ void __launch_bounds__(32 * WARP_CTA_WARPS, (WarpCfg<NT, QT, MODE>::MINB))
+__global__ void __launch_bounds__(32 * WarpCfg<NT, QT, MODE>::W, (WarpCfg<NT, QT, MODE>::MINB_))
 k_warp(ElemArgs A) {
   using TR = ModeTraits<MODE>;
   using CF = WarpCfg<NT, QT, MODE>;
@@ -199,8 +210,9 @@ k_warp(ElemArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
   double* sTile = sT + NP * QP + warp * (NSTAGE > 0 ? NSTAGE * TILE : 0);
-  double* sW = sT + NP * QP + WARP_CTA_WARPS * NSTAGE * TILE + warp * WDBL;   // [rt][ht][w][lane][2]
-  double* sInv = sT + NP * QP + WARP_CTA_WARPS * (NSTAGE * TILE + WDBL);      // 1/(2k+1), k < NP
+  constexpr int W = CF::W, NBUF = CF::PIPE ? 2 : 1;
+  double* sW = sT + NP * QP + W * NSTAGE * TILE + warp * NBUF * WDBL;   // [buf][rt][ht][w][lane][2]
+  double* sInv = sT + NP * QP + W * (NSTAGE * TILE + NBUF * WDBL);      // 1/(2k+1), k < NP
   // tables: every copy in flight at once (cp.async, no register staging)
   for (int i = 2 * threadIdx.x; i < QP * NP; i += 2 * blockDim.x) {
     cp_async16(sS + i, A.Sf + i);
@@ -212,26 +224,29 @@ k_warp(ElemArgs A) {
   // grid-dependency wait.  This is safe because no PDL kernel that writes a
   // weight cache triggers its dependents early (the residual modes below), so
   // a weight cache is always complete when a kernel reading it is launched.
-  auto load_weights = [&](int e) {
+  int buf = 0;
+  auto load_weights = [&](int e, int b) {
     if constexpr (WSMEM) {
       const double* src = A.wc_in + wc_index(e, QT, 0, 0, NW, 0, lane);
+      double* dst = sW + b * WDBL;
 #pragma unroll
-      for (int t = 0; t < QT * QT * NW; ++t) cp_async16(sW + t * 64 + 2 * lane, src + t * 64);
+      for (int t = 0; t < QT * QT * NW; ++t) cp_async16(dst + t * 64 + 2 * lane, src + t * 64);
       cp_async_commit();
     }
   };
-  const int stride = gridDim.x * WARP_CTA_WARPS;
-  int e = blockIdx.x * WARP_CTA_WARPS + warp;
-  if (e < A.N) load_weights(e);
+  const int stride = gridDim.x * W;
+  int e = blockIdx.x * W + warp;
+  if (e < A.N) load_weights(e, 0);
   // one wave: let the next kernel in the stream start its prologue now --
   // except kernels that write a weight cache (see load_weights)
   if constexpr (!CF::WRITES_WC) pdl_trigger();
   pdl_wait();
 
-  double X[REGX ? NIN : 1][REGX ? NK : 1][REGX ? NT : 1];
+  using XFrag = double[REGX ? NIN : 1][REGX ? NK : 1][REGX ? NT : 1];
+  XFrag X, Xn;
   // issue the loads of cell e: the first contraction's B fragments (registers
   // or the warp's staging tile)
-  auto load_cell = [&](int e) {
+  auto load_cell = [&](int e, XFrag& Xd) {
     const int cx = e / A.ncy, cy = e - cx * A.ncy;
     if constexpr (REGX) {
 #pragma unroll
@@ -246,7 +261,7 @@ k_warp(ElemArgs A) {
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const int b = 8 * nt + r;
-            X[f][ks][nt] = (a < A.n && b < A.n) ? __ldg(src + (long long)a * A.ld + b) : 0.0;
+            Xd[f][ks][nt] = (a < A.n && b < A.n) ? __ldg(src + (long long)a * A.ld + b) : 0.0;
           }
         }
       }
@@ -266,13 +281,29 @@ k_warp(ElemArgs A) {
       }
     }
   };
-  if (e < A.N) load_cell(e);
-  cp_async_wait_all();
+  if (e < A.N) load_cell(e, X);
+  if constexpr (CF::PIPE) {
+    // tables (first group) must be in; the cell's weights may still fly
+    if (e < A.N) cp_async_wait_group<1>();
+    else cp_async_wait_all();
+  } else {
+    cp_async_wait_all();
+  }
   __syncthreads();   // tables
 
   for (; e < A.N; e += stride) {
     const int cx = e / A.ncy, cy = e - cx * A.ncy;
     if constexpr (!REGX) __syncwarp();
+    bool more = false;
+    if constexpr (CF::PIPE) {
+      // next cell's weights and x fragments in flight during this cell
+      more = e + stride < A.N;
+      if (more) {
+        load_weights(e + stride, buf ^ 1);
+        load_cell(e + stride, Xn);
+      }
+    }
+    const double* sWc = sW + buf * WDBL;
     double Y[NOUT][NT][NT][2];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
@@ -320,11 +351,14 @@ k_warp(ElemArgs A) {
         for (int f = 0; f < NSYN; ++f) { Vp[f][0] = V[f][ht][0]; Vp[f][1] = V[f][ht][1]; }
         double out2[NOUT][2];
         if constexpr (WSMEM) {
-          if (rt == 0 && ht == 0) cp_async_wait_all();
+          if (rt == 0 && ht == 0) {
+            if (more) cp_async_wait_group<1>();
+            else cp_async_wait_all();
+          }
           double Wc[NW][2];
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            const double2 t = *reinterpret_cast<const double2*>(sW + ((rt * QT + ht) * NW + w) * 64 + 2 * lane);
+            const double2 t = *reinterpret_cast<const double2*>(sWc + ((rt * QT + ht) * NW + w) * 64 + 2 * lane);
             Wc[w][0] = t.x;
             Wc[w][1] = t.y;
           }
@@ -358,9 +392,21 @@ k_warp(ElemArgs A) {
       if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
     }
     // REGX / cp.async: the next cell's loads are in flight during the epilogue
-    if (e + stride < A.N) load_weights(e + stride);
-    if constexpr (REGX) {
-      if (e + stride < A.N) load_cell(e + stride);
+    if constexpr (CF::PIPE) {
+      if (more) {
+#pragma unroll
+        for (int f = 0; f < NIN; ++f)
+#pragma unroll
+          for (int ks = 0; ks < NK; ++ks)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) X[f][ks][nt] = Xn[f][ks][nt];
+      }
+      buf ^= 1;
+    } else {
+      if (e + stride < A.N) load_weights(e + stride, 0);
+      if constexpr (REGX) {
+        if (e + stride < A.N) load_cell(e + stride, X);
+      }
     }
 #pragma unroll
     for (int o = 0; o < NOUT; ++o)
@@ -375,7 +421,7 @@ k_warp(ElemArgs A) {
           }
     if constexpr (!REGX) {
       __syncwarp();
-      if (e + stride < A.N) load_cell(e + stride);
+      if (e + stride < A.N) load_cell(e + stride, X);
     }
   }
 }

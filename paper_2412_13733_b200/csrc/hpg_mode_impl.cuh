@@ -13,9 +13,11 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
   constexpr int NP = 8 * NT, QP = 8 * QT;
   constexpr int NSTAGE = WarpCfg<NT, QT, MODE>::REGX ? 0 : TR::NIN;
-  constexpr int WDBL = WarpCfg<NT, QT, MODE>::WSMEM ? WarpCfg<NT, QT, MODE>::WDBL : 0;
-  const size_t smem = sizeof(double) * (2 * QP * NP + WARP_CTA_WARPS * (NSTAGE * NP * (NP + 2) + WDBL) + NP +
-                                        (size_t)WARP_CTA_WARPS * A.usmem);
+  using CF = WarpCfg<NT, QT, MODE>;
+  constexpr int W = CF::W;
+  constexpr int WDBL = CF::WSMEM ? CF::WDBL * (CF::PIPE ? 2 : 1) : 0;
+  const size_t smem = sizeof(double) * (2 * QP * NP + W * (NSTAGE * NP * (NP + 2) + WDBL) + NP +
+                                        (size_t)W * A.usmem);
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "warp path shared memory too large");
   static size_t attr = 0;
   if (smem > attr) {
@@ -29,17 +31,17 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp<NT, QT, MODE>, 32 * WARP_CTA_WARPS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp<NT, QT, MODE>, 32 * W, smem);
     if (occ < 1) occ = 1;
     occ_smem = (int)smem;
   }
-  int need = (A.N + WARP_CTA_WARPS - 1) / WARP_CTA_WARPS;
+  int need = (A.N + W * CF::CPW - 1) / (W * CF::CPW);
   int grid = need < nsm * occ ? need : nsm * occ;
   // programmatic dependent launch: the table prologue overlaps the previous
   // kernel's tail (k_warp orders its data reads with griddepcontrol.wait)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(32 * WARP_CTA_WARPS);
+  cfg.blockDim = dim3(32 * W);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];

@@ -474,14 +474,19 @@ __device__ __forceinline__ Sp3 k_row(int j, Inv inv_odd) {
 }
 
 template <bool GRADIENT>
-__global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG) {
-  // cpb cell groups of TG threads per CTA (small tiles share a CTA)
+__global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG, int usplit) {
+  // cpb cell groups of TG threads per CTA (small tiles share a CTA); with few
+  // large cells (cpb == 1, config 3) usplit CTAs share one cell's entries
+  // (each stages the whole tile, then takes every usplit-th block of TG)
   extern __shared__ double smem[];
   const int m = A.m, n = A.n, p = A.p, ld = m | 1;
-  const int grp = threadIdx.x / TG, t0 = threadIdx.x - grp * TG;
+  const int grp = threadIdx.x / TG;
+  const int sp = blockIdx.x % usplit;
+  const int t0 = threadIdx.x - grp * TG;
+  const int tstart = t0 + sp * TG, tstep = TG * usplit;
   double* sI = smem;                                   // 1/(2k+1)
   for (int t = threadIdx.x; t < 2 * m + 8; t += blockDim.x) sI[t] = kInvOdd[t];
-  const int e = blockIdx.x * cpb + grp;
+  const int e = (blockIdx.x / usplit) * cpb + grp;
   const bool valid = grp < cpb && e < A.N;
   const int ee = valid ? e : 0;
   const int cx = ee / A.ncy, cy = ee - cx * A.ncy;
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG) 
   __syncthreads();
   auto C = [&](int i, int l) { return sC[i * ld + l]; };
   auto inv = [&](int k) { return sI[k]; };
-  for (int t = valid ? t0 : m * m; t < m * m; t += TG) {
+  for (int t = valid ? tstart : m * m; t < m * m; t += tstep) {
     const int j = t / m, k = t - j * m;
     // A u (local) = (hy/hx) Kref C Mref + (hx/hy) Mref C Kref,
     // Mref = R^T diag(1/(2l+1)) R expanded as nested sparse sums
