@@ -63,6 +63,9 @@ struct ElemArgs {
   int NT, QT, splits;
   double* partial;   // [N][splits][NOUT][NP*NP] when splits > 1
   int out_cellmajor; // M_VALUES for the u side: out is (N, n, n) cell-major
+  int smem_tables;   // CTA path: PK(S), PK(T) staged in shared memory
+  int cluster_red;   // CTA path, splits > 1: the split CTAs of a cell form a
+                     // thread-block cluster and reduce through DSMEM
   // fused residual U side (hpg_ucell.cuh)
   double alpha;
   const double* psi_prev;

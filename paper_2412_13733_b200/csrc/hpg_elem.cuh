@@ -11,6 +11,8 @@
 // and M[a][b] = w_a w_b Y[b][a] (reference CellKernel2D.moments,
 // assembly.py:249-251).  Zero-padded tables make the padded rows/cols inert.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "hpg_common.cuh"
 #include "hpg_pointmap.cuh"
 #include "hpg_ucell.cuh"
@@ -448,6 +450,21 @@ k_cta(ElemArgs A) {
   const int r = lane >> 2, c = lane & 3;
   const int e = blockIdx.x / A.splits, sp = blockIdx.x - e * A.splits;
   if (e >= A.N) return;
+  // table operands: shared memory when they fit (config 2), else L1/L2
+  const double* tS = A.Sf;
+  const double* tT = A.Tf;
+  if (A.smem_tables) {
+    double* s0 = sR + NOUT * NT * 64;
+    double* s1 = s0 + QT * NP * 8;
+    for (int i = 2 * threadIdx.x; i < QT * NP * 8; i += 2 * blockDim.x) {
+      cp_async16(s0 + i, A.Sf + i);
+      cp_async16(s1 + i, A.Tf + i);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    tS = s0;
+    tT = s1;
+  }
   const int rt0 = (sp * QT) / A.splits, rt1 = ((sp + 1) * QT) / A.splits;
   const int cx = e / A.ncy, cy = e - cx * A.ncy;
 
@@ -474,12 +491,16 @@ k_cta(ElemArgs A) {
     // (1) P tiles
     for (int it = warp; it < NSYN * NT; it += CTA_WARPS) {
       int f = it / NT, nt = it - f * NT;
-      double P[2] = {0.0, 0.0};
+      // two independent accumulation chains (even / odd k-steps): half the
+      // dependent DMMA latency per tile (NK = 2 NT is even)
+      double P[2] = {0.0, 0.0}, P1[2] = {0.0, 0.0};
       const double* col = sTile + f * TILE + 8 * nt + r;
-      #pragma unroll 8
-      for (int ks = 0; ks < NK; ++ks)
-        dmma(P, __ldg(A.Sf + (rt * NK + ks) * 32 + lane), col[(8 * (ks >> 1) + 2 * c + (ks & 1)) * LDT]);
-      *reinterpret_cast<double2*>(sP + (f * NT + nt) * 64 + 2 * lane) = make_double2(P[0], P[1]);
+      #pragma unroll 4
+      for (int ks = 0; ks < NK; ks += 2) {
+        dmma(P, tS[(rt * NK + ks) * 32 + lane], col[(8 * (ks >> 1) + 2 * c) * LDT]);
+        dmma(P1, tS[(rt * NK + ks + 1) * 32 + lane], col[(8 * (ks >> 1) + 2 * c + 1) * LDT]);
+      }
+      *reinterpret_cast<double2*>(sP + (f * NT + nt) * 64 + 2 * lane) = make_double2(P[0] + P1[0], P[1] + P1[1]);
     }
     __syncthreads();
     // (2) V tiles + pointwise map
@@ -487,13 +508,16 @@ k_cta(ElemArgs A) {
       double V[NSYN > 0 ? NSYN : 1][2];
 #pragma unroll
       for (int f = 0; f < NSYN; ++f) {
+        double V1[2] = {0.0, 0.0};
         V[f][0] = V[f][1] = 0.0;
-        #pragma unroll 8
+        #pragma unroll 4
         for (int t = 0; t < NT; ++t) {
           double2 pa = *reinterpret_cast<const double2*>(sP + (f * NT + t) * 64 + 2 * lane);
-          dmma(V[f], pa.x, __ldg(A.Sf + (ht * NK + 2 * t) * 32 + lane));
-          dmma(V[f], pa.y, __ldg(A.Sf + (ht * NK + 2 * t + 1) * 32 + lane));
+          dmma(V[f], pa.x, tS[(ht * NK + 2 * t) * 32 + lane]);
+          dmma(V1, pa.y, tS[(ht * NK + 2 * t + 1) * 32 + lane]);
         }
+        V[f][0] += V1[0];
+        V[f][1] += V1[1];
       }
       double out2[NOUT][2];
       map_pair<MODE, NSYN, NOUT, NW>(A, e, QT, rt, ht, lane, V, out2, flag);
@@ -505,14 +529,14 @@ k_cta(ElemArgs A) {
     // (3) R tiles
     for (int it = warp; it < NOUT * NT; it += CTA_WARPS) {
       int o = it / NT, bt = it - o * NT;
-      double R[2] = {0.0, 0.0};
-      #pragma unroll 8
+      double R[2] = {0.0, 0.0}, R1[2] = {0.0, 0.0};
+      #pragma unroll 4
       for (int t = 0; t < QT; ++t) {
         double2 vb = *reinterpret_cast<const double2*>(sV + (o * QT + t) * 64 + 2 * lane);
-        dmma(R, __ldg(A.Tf + (bt * QK + 2 * t) * 32 + lane), vb.x);
-        dmma(R, __ldg(A.Tf + (bt * QK + 2 * t + 1) * 32 + lane), vb.y);
+        dmma(R, tT[(bt * QK + 2 * t) * 32 + lane], vb.x);
+        dmma(R1, tT[(bt * QK + 2 * t + 1) * 32 + lane], vb.y);
       }
-      *reinterpret_cast<double2*>(sR + (o * NT + bt) * 64 + 2 * lane) = make_double2(R[0], R[1]);
+      *reinterpret_cast<double2*>(sR + (o * NT + bt) * 64 + 2 * lane) = make_double2(R[0] + R1[0], R[1] + R1[1]);
     }
     __syncthreads();
     // (4) Y accumulation (tiles statically owned by warps)
@@ -523,13 +547,47 @@ k_cta(ElemArgs A) {
         int o = it / (NT * NT), rem = it - o * NT * NT;
         int bt = rem / NT, at = rem - bt * NT;
         double2 ra = *reinterpret_cast<const double2*>(sR + (o * NT + bt) * 64 + 2 * lane);
-        dmma(Y[s], ra.x, __ldg(A.Tf + (at * QK + 2 * rt) * 32 + lane));
-        dmma(Y[s], ra.y, __ldg(A.Tf + (at * QK + 2 * rt + 1) * 32 + lane));
+        dmma(Y[s], ra.x, tT[(at * QK + 2 * rt) * 32 + lane]);
+        dmma(Y[s], ra.y, tT[(at * QK + 2 * rt + 1) * 32 + lane]);
       }
     }
   }
   if constexpr (MODE == M_OBST_RES) {
     if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
+  }
+  if (A.cluster_red) {
+    // the A.splits CTAs of cell e are one cluster: stage this CTA's partial
+    // Y in its own shared memory, then CTA sp reduces a slice of the entries
+    // over the cluster's partials through DSMEM in split order (the same
+    // deterministic sum as k_cta_reduce), with no global partials and no
+    // second launch
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __syncthreads();                       // tile / stage buffers are dead
+    double* sY = smem;                     // [NOUT][NP][NP]
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) {
+      int it = warp + CTA_WARPS * s;
+      if (it < ny) {
+        int o = it / (NT * NT), rem = it - o * NT * NT;
+        int bt = rem / NT, at = rem - bt * NT;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sY[(o * NP + 8 * at + 2 * c + j) * NP + 8 * bt + r] = Y[s][j];
+      }
+    }
+    cl.sync();
+    const int nn = A.n * A.n, total = NOUT * nn;
+    const int chunk = (total + A.splits - 1) / A.splits;
+    const int i1 = min(total, (sp + 1) * chunk);
+    for (int idx = sp * chunk + threadIdx.x; idx < i1; idx += blockDim.x) {
+      const int o = idx / nn, rem = idx - o * nn, a = rem / A.n, b = rem - a * A.n;
+      const int off = (o * NP + a) * NP + b;
+      double y = 0.0;
+      for (int q = 0; q < A.splits; ++q) y += cl.map_shared_rank(sY, q)[off];
+      write_moment<MODE>(A, e, cx, cy, o, a, b, y);
+    }
+    cl.sync();                             // partials stay alive until read
+    return;
   }
 #pragma unroll
   for (int s = 0; s < MAXS; ++s) {

@@ -1,6 +1,7 @@
 // Instantiation body shared by the hpg_mode_*.cu translation units.
 // Define HPG_MODE and the warp (NT, QT) list (HPG_WARP_LIST) before including.
 #pragma once
+#include <cstdio>
 #include <cstdlib>
 #include "hpg_elem.cuh"
 #include "hpg_launch.cuh"
@@ -61,12 +62,64 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
   const int NP = 8 * A.NT;
   size_t smem = sizeof(double) * ((size_t)TR::NIN * NP * (NP + 2) +
                                   (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64);
+  // stage the tables too when the CTA still fits twice per SM
+  const size_t tsmem = sizeof(double) * (size_t)2 * (8 * A.QT) * NP;
+  A.smem_tables = (smem + tsmem) <= 100 * 1024 && getenv("HPG_NO_SMEM_TABLES") == nullptr;
+  if (A.smem_tables) smem += tsmem;
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "element tile too large for shared memory");
   static int attr = 0;
   if ((int)smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_cta)", e);
     attr = (int)smem;
+  }
+  // row-tile splits of a cell as one thread-block cluster (<= 8, portable):
+  // partials reduced through DSMEM inside the kernel, when the clusters fit
+  // in one wave (checked once per shape)
+  A.cluster_red = 0;
+  if (A.splits > 1 && A.splits <= 8 && getenv("HPG_NO_CLUSTER") == nullptr) {
+    const size_t ysmem = sizeof(double) * (size_t)TR::NOUT * NP * NP;
+    const size_t csmem = smem > ysmem ? smem : ysmem;
+    static int ok_splits = -1, ok_n = -1, ok_np = -1, ok_res = 0;
+    if (ok_splits != A.splits || ok_n != A.N || ok_np != NP) {
+      ok_splits = A.splits; ok_n = A.N; ok_np = NP; ok_res = 0;
+      if (csmem <= 227 * 1024 &&
+          cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem) == cudaSuccess) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(A.N * A.splits);
+        q.blockDim = dim3(32 * W);
+        q.dynamicSmemBytes = csmem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = A.splits; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        int nclusters = 0;
+        cudaError_t qe = cudaOccupancyMaxActiveClusters(&nclusters, k_cta<MODE, MAXS, W>, &q);
+        if (qe == cudaSuccess && nclusters >= A.N) ok_res = 1;
+        if (getenv("HPG_DEBUG"))
+          fprintf(stderr, "[hpg] k_cta mode %d: %d cells x %d splits, smem %zu: max active clusters %d (%s) -> %s\n",
+                  MODE, A.N, A.splits, csmem, nclusters, cudaGetErrorString(qe), ok_res ? "cluster" : "reduce kernel");
+        cudaGetLastError();
+        if ((int)csmem > attr) attr = (int)csmem;
+      }
+    }
+    if (ok_res) {
+      A.cluster_red = 1;
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(A.N * A.splits);
+      q.blockDim = dim3(32 * W);
+      q.dynamicSmemBytes = smem > ysmem ? smem : ysmem;
+      q.stream = s;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = A.splits; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&q, k_cta<MODE, MAXS, W>, A);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_cta cluster launch", e);
+    }
   }
   k_cta<MODE, MAXS, W><<<A.N * A.splits, 32 * W, smem, s>>>(A);
   cudaError_t e = cudaGetLastError();

@@ -1,0 +1,64 @@
+"""GPU: the alternative launch paths of one operation agree.
+
+* CTA path with row-tile splits: the cluster (DSMEM) reduction and the
+  separate reduction kernel sum the split partials in the same order, so
+  residual moments and cached applies are bitwise identical; both match the
+  oracle at 1e-12 (few cells -> splits <= 8 -> cluster launch).
+* CTA path with / without the shared-memory table copies: identical.
+* Low-degree single-pass residual (k_lowp) vs the three-kernel path
+  (U side + psi side + hat gather): same results to 1e-12 (different
+  summation order of the hat contributions)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import hpg_oracle as orc
+from test_gpu_fullsize import build  # noqa: E402  (tests/ is on sys.path under pytest)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _with_env(var, fn):
+    os.environ[var] = "1"
+    try:
+        return fn()
+    finally:
+        del os.environ[var]
+
+
+@pytest.mark.parametrize("cfg_name,ncells", [("c2", 2), ("c2", 3), ("c3", 2)])
+def test_cta_split_reduction_paths(cfg_name, ncells):
+    cfg, d, P, inp, dev = build(cfg_name, ncells=ncells)
+    alpha = cfg.alphas[0]
+
+    def run():
+        b_u, b_psi, _ = d.residual_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
+        y = d.apply_cached_t(dev["x"])
+        return b_psi.cpu().numpy(), y.cpu().numpy()
+
+    a_psi, a_y = run()
+    b_psi, b_y = _with_env("HPG_NO_CLUSTER", run)
+    c_psi, c_y = _with_env("HPG_NO_SMEM_TABLES", run)
+    assert np.array_equal(a_psi, b_psi) and np.array_equal(a_y, b_y)
+    assert np.array_equal(a_psi, c_psi) and np.array_equal(a_y, c_y)
+    ry = (P.obstacle_apply_D(inp["psi"], inp["x"]) if cfg.kind == "obstacle"
+          else P.gradient_apply_D(inp["psi"], inp["x"], P.sample(inp["phi"])))
+    assert orc.rel_err(a_y, ry) < TOL
+
+
+@pytest.mark.parametrize("cfg_name", ["c4p2", "c4p4", "c4p6"])
+def test_lowp_single_pass_vs_three_kernels(cfg_name):
+    cfg, d, P, inp, dev = build(cfg_name, ncells=37)
+    alpha = cfg.alphas[0]
+
+    def run():
+        b_u, b_psi, y, flag = d.residual_apply_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], dev["x"])
+        return b_u.cpu().numpy(), b_psi.cpu().numpy(), y.cpu().numpy(), int(flag.item())
+
+    one = run()
+    three = _with_env("HPG_LOWP_OFF", run)
+    for a, b in zip(one[:3], three[:3]):
+        assert orc.rel_err(a, b) < TOL
+    assert one[3] == three[3]
