@@ -183,7 +183,8 @@ def config_dict(cfg, rule):
 
 # dram bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (cold caches: ncu flushes L2 between replays), see profiles/
-NCU_TRAFFIC = {("c1", "gauss"): (26323968.0, "profiles/r01_ncu_full_c1_apply.txt")}
+NCU_TRAFFIC = {("c1", "gauss"): (26274816.0, "profiles/r01b_ncu_full_c1_apply.txt"),
+               ("c4p6", "gauss"): (90302464.0 + 22354176.0, "profiles/r01b_ncu_full_c4p6_lowp.txt")}
 
 
 def run_reference(args, cfg, rank, world):
@@ -399,7 +400,7 @@ def main():
     torch.cuda.synchronize()
 
     launches_per_residual = 3 + (1 if disc.plan.splits > 1 and disc.plan.path == 1 else 0)
-    launches_per_step = (launches_per_residual + kmv) if cached else 3 * reps
+    launches_per_step = (launches_per_residual + kmv) if cached else disc.plan.residual_apply_kernels * reps
 
     def run_steps(nsteps, timed):
         evs = []
@@ -454,9 +455,11 @@ def main():
         t_k = statistics.mean(res_ms) / reps * 1e-3       # fused residual + apply per rep
         bytes_ = B_res + B_mv
         achieved = bytes_ / t_k / 1e9
-        roof = {"kernel": "fused residual + apply per rep (k_uside_pt + k_small<n,Q,res,apply> + k_hat_gather)",
+        roof = {"kernel": "k_lowp<p,Q,apply> (single-pass residual + Jacobian apply, one launch per rep)",
                 "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm,
+                "traffic": NCU_TRAFFIC.get((cfg.name, rule), (None, None))[0],
+                "traffic_source": NCU_TRAFFIC.get((cfg.name, rule), (None, "not captured for this config"))[1],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "algorithmic_per_launch": {"flops": F_res + F_mv, "bytes": bytes_},
                 "avg_launch_us": t_k * 1e6}
@@ -524,14 +527,19 @@ def main():
         precond = precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm)
 
     # Schur-reduced Newton linear solve on the device
+    # (needs the per-cell preconditioner: config 3's 6561^2 blocks exceed the
+    # per-CTA LU, hpgLUMaxBlock, and are reported as unsupported, not timed)
+    lu_fits = cfg.ncomp * disc.n * disc.n <= _lib.load().hpgLUMaxBlock()
     schur_info = None
     if world == 1 and disc.plan.ndof_u > 0:
-        schur_info = schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag)
+        schur_info = (schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag) if lu_fits else
+                      {"unsupported": "per-cell LU block side exceeds hpgLUMaxBlock()"})
 
     # the whole penalty continuation (proximal.solve) on the device, obstacle configs
     solve_info = None
     if world == 1 and cfg.kind == "obstacle":
-        solve_info = solve_timing(disc)
+        solve_info = (solve_timing(disc) if lu_fits else
+                      {"unsupported": "per-cell LU block side exceeds hpgLUMaxBlock()"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

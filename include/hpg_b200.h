@@ -53,8 +53,10 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq,
                   const double* S, const double* T, const double* Su,
                   const double* Tu, const double* hx, const double* hy);
 int hpgPlanDestroy(hpgPlan plan);
-/* info[0..9] = n, m, nq, ncells, ndof_psi, ndof_u, wcache_doubles,
- *              block_doubles_per_cell, path(0 warp, 1 cta), splits */
+/* info[0..10] = n, m, nq, ncells, ndof_psi, ndof_u, wcache_doubles,
+ *               block_doubles_per_cell, path(0 warp, 1 cta), splits,
+ *               kernels per hpgResidualApply call (1: single-pass path).
+ * info must hold at least 11 entries. */
 int hpgPlanInfo(hpgPlan plan, long long* info);
 
 /* ObstacleDisc2D.exp_moments (assembly.py:541-548).  out[ndof_psi].

@@ -335,6 +335,9 @@ int hpgPlanInfo(hpgPlan P, long long* info) {
   info[7] = nb * nb;
   info[8] = P->kind == HPG_OBSTACLE ? (P->use_warp[M_OBST_RES] ? 0 : 1) : (P->use_warp[M_GRAD_RES] ? 0 : 1);
   info[9] = P->splits;
+  // kernels per fused residual + apply call: 1 on the single-pass low-degree
+  // path (k_lowp), else U side + psi side + hat gather (+ apply)
+  info[10] = (P->kind == HPG_OBSTACLE && P->small && lowp_available(P->p, P->nq)) ? 1 : 3;
   return HPG_OK;
 }
 
