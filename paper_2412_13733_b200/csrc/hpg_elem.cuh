@@ -160,7 +160,18 @@ __device__ __forceinline__ void map_pair_w(const double (&V)[NSYN > 0 ? NSYN : 1
 template <int NT, int QT, int MODE>
 struct WarpCfg {
   using TR = ModeTraits<MODE>;
-  static constexpr bool REGX = TR::NIN * 2 * NT * NT <= (MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED ? 8 : 4);
+#ifndef HPG_REGX_CACHED
+#define HPG_REGX_CACHED 8
+#endif
+#ifndef HPG_SPLIT_R
+#define HPG_SPLIT_R 0
+#endif
+#ifndef HPG_SPLIT_V
+#define HPG_SPLIT_V 0
+#endif
+  static constexpr bool REGX = TR::NIN * 2 * NT * NT <= (MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED ? HPG_REGX_CACHED : 4);
+  // independent even/odd accumulation chains in the R / V contractions
+  static constexpr bool SPLIT_R = HPG_SPLIT_R, SPLIT_V = HPG_SPLIT_V;
   static constexpr bool cached = MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED;
   // cached modes: the cell's point weights are copied to shared memory with
   // cp.async when they fit (<= 16 KB per warp), read back by the same lane
@@ -340,9 +351,20 @@ k_warp(ElemArgs A) {
 #pragma unroll
         for (int ht = 0; ht < QT; ++ht) {
           V[f][ht][0] = V[f][ht][1] = 0.0;
+          if constexpr (CF::SPLIT_V) {
+            double V1[2] = {0.0, 0.0};
 #pragma unroll
-          for (int ks = 0; ks < NK; ++ks)
-            dmma(V[f][ht], P[ks >> 1][ks & 1], sS[(ht * NK + ks) * 32 + lane]);
+            for (int ks = 0; ks < NK; ks += 2) {
+              dmma(V[f][ht], P[ks >> 1][0], sS[(ht * NK + ks) * 32 + lane]);
+              dmma(V1, P[ks >> 1][1], sS[(ht * NK + ks + 1) * 32 + lane]);
+            }
+            V[f][ht][0] += V1[0];
+            V[f][ht][1] += V1[1];
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < NK; ++ks)
+              dmma(V[f][ht], P[ks >> 1][ks & 1], sS[(ht * NK + ks) * 32 + lane]);
+          }
         }
       }
       double Vw[NOUT][QT][2];
@@ -377,9 +399,21 @@ k_warp(ElemArgs A) {
 #pragma unroll
         for (int bt = 0; bt < NT; ++bt) {
           R[bt][0] = R[bt][1] = 0.0;
+          if constexpr (CF::SPLIT_R) {
+            // two independent chains (even / odd k-steps)
+            double R1[2] = {0.0, 0.0};
 #pragma unroll
-          for (int ks = 0; ks < QK; ++ks)
-            dmma(R[bt], sT[(bt * QK + ks) * 32 + lane], Vw[o][ks >> 1][ks & 1]);
+            for (int ks = 0; ks < QK; ks += 2) {
+              dmma(R[bt], sT[(bt * QK + ks) * 32 + lane], Vw[o][ks >> 1][0]);
+              dmma(R1, sT[(bt * QK + ks + 1) * 32 + lane], Vw[o][ks >> 1][1]);
+            }
+            R[bt][0] += R1[0];
+            R[bt][1] += R1[1];
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < QK; ++ks)
+              dmma(R[bt], sT[(bt * QK + ks) * 32 + lane], Vw[o][ks >> 1][ks & 1]);
+          }
         }
 #pragma unroll
         for (int bt = 0; bt < NT; ++bt)

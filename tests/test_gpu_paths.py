@@ -62,3 +62,21 @@ def test_lowp_single_pass_vs_three_kernels(cfg_name):
     for a, b in zip(one[:3], three[:3]):
         assert orc.rel_err(a, b) < TOL
     assert one[3] == three[3]
+
+
+@pytest.mark.parametrize("n", [1000, 921600, 921601])
+def test_host_transfers_roundtrip(n):
+    """NumPy <-> device through the API's staging (direct below 1 MB, two
+    pinned half buffers above): exact, repeated, interleaved with kernels."""
+    import torch
+    cfg, d, P, inp, dev = build("c4p2", ncells=4)
+    rng = np.random.default_rng(n)
+    for rep in range(3):
+        a = rng.standard_normal(n)
+        t = d.h2d(a, f"rt{rep % 2}")
+        b = rng.standard_normal(n)
+        t2 = d.h2d(b, "rt_other")
+        s = (t * 2.0 + t2).clone()
+        torch.cuda.synchronize()
+        assert np.array_equal(d.d2h(t, "rt"), a)
+        assert np.array_equal(d.d2h(s, "rt2"), a * 2.0 + b)
