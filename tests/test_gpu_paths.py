@@ -80,3 +80,18 @@ def test_host_transfers_roundtrip(n):
         torch.cuda.synchronize()
         assert np.array_equal(d.d2h(t, "rt"), a)
         assert np.array_equal(d.d2h(s, "rt2"), a * 2.0 + b)
+
+
+@pytest.mark.parametrize("cfg_name,ncells", [("c1", 64), ("c1", 3), ("c2", 5), ("c3", 2), ("c4p4", 33)])
+def test_host_pipelined_matvec(cfg_name, ncells):
+    """``D @ x`` with NumPy arrays (pinned half-buffer staging both ways)
+    equals the device apply bitwise, repeatedly."""
+    cfg, d, P, inp, dev = build(cfg_name, ncells=ncells)
+    D = d.assemble_D(inp["psi"])
+    ref = d.apply_cached_t(dev["x"]).cpu().numpy()
+    for _ in range(3):
+        assert np.array_equal(D @ inp["x"], ref)
+    x2 = np.random.default_rng(1).standard_normal(d.ndof_psi)
+    import torch
+    ref2 = d.apply_cached_t(torch.from_numpy(x2).cuda()).cpu().numpy()
+    assert np.array_equal(D @ x2, ref2)
