@@ -417,10 +417,13 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     if (x != nullptr) { A.in1 = x; A.wc_out = y; }
     return run_lowp(P->p, P->nq, x != nullptr, A, P->stab, s);
   }
-  if (usmall_available(P->p, P->kind == HPG_GRADIENT)) {
+  // thread-per-cell U side only when there are enough cells to fill the GPU;
+  // few cells (config 0: 16) go to the thread-per-entry kernel below
+  const bool many = P->N >= 8 * P->nsm;
+  if (many && usmall_available(P->p, P->kind == HPG_GRADIENT)) {
     // (1) U side, low degree: thread per cell, generated straight-line code
     if ((rc = run_usmall(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
-  } else if (P->kind == HPG_OBSTACLE && upass_available(P->p) && getenv("HPG_UPASS_OFF") == nullptr) {
+  } else if (many && P->kind == HPG_OBSTACLE && upass_available(P->p) && getenv("HPG_UPASS_OFF") == nullptr) {
     // (1) U side, mid degree: warp per cell, generated separable passes
     if ((rc = run_upass(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
   } else {
@@ -428,6 +431,9 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     //     (obstacle) | -B^T u (gradient); b_u on owned dofs + edge scratch
     int TG = P->m * P->m;
     TG = TG > 1024 ? 1024 : ((TG + 31) / 32) * 32;
+    // many mid-size cells (config 2): two entries per thread, so >= 2 CTAs
+    // fit an SM (register-limited) and all cells run in one wave
+    if (P->N >= P->nsm && TG > 512) TG = ((P->m * P->m + 1) / 2 + 31) / 32 * 32;
     int cpb = 256 / TG;
     if (cpb < 1) cpb = 1;
     size_t smem = sizeof(double) * ((size_t)cpb * ((size_t)P->m * (P->m | 1) + 2 * (size_t)P->n * P->n) +
