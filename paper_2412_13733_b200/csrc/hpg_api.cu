@@ -450,8 +450,12 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
       if (usplit > blocks) usplit = blocks;
       if (usplit < 1) usplit = 1;
     }
-    void* args[] = {&U, &cpb, &TG, &usplit};
-    CUDA_TRY(cudaLaunchKernel(fn, dim3((P->N + cpb - 1) / cpb * usplit), dim3(cpb * TG), args, smem, s));
+    if (P->kind == HPG_GRADIENT)
+      CUDA_TRY(launch_pdl(k_uside_pt<true>, dim3((P->N + cpb - 1) / cpb * usplit), dim3(cpb * TG), smem, s, U, cpb,
+                          TG, usplit));
+    else
+      CUDA_TRY(launch_pdl(k_uside_pt<false>, dim3((P->N + cpb - 1) / cpb * usplit), dim3(cpb * TG), smem, s, U, cpb,
+                          TG, usplit));
     CUDA_TRY(cudaGetLastError());
   }
   // (2) psi side finishes b_psi in place (proximal.py:123 order)
@@ -470,7 +474,7 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
   if (rc) return rc;
   long long nh = (long long)(P->ncx - 1) * P->niy + (long long)(P->nix - (P->ncx - 1)) * (P->ncy - 1);
   if (nh > 0) {
-    k_hat_gather<<<(unsigned)((nh + 255) / 256), 256, 0, s>>>(A);
+    CUDA_TRY(launch_pdl(k_hat_gather, dim3((unsigned)((nh + 255) / 256)), dim3(256), 0, s, A));
     CUDA_TRY(cudaGetLastError());
   }
   if (x != nullptr) {

@@ -195,8 +195,6 @@ struct WarpCfg {
   static constexpr bool UNROLL_RT = HPG_UNROLL_RT && cached && QT <= 3;
 };
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
@@ -470,6 +468,7 @@ k_warp(ElemArgs A) {
 template <int MODE, int MAXS, int CTA_WARPS>
 __global__ void __launch_bounds__(32 * CTA_WARPS, 1)
 k_cta(ElemArgs A) {
+  pdl_wait();
   using TR = ModeTraits<MODE>;
   constexpr int NIN = TR::NIN, NSYN = TR::NSYN, NOUT = TR::NOUT, NW = TR::NW;
   const int NT = A.NT, QT = A.QT;
@@ -645,6 +644,7 @@ k_cta(ElemArgs A) {
 // Deterministic reduction of the row-tile-split partials + epilogue.
 template <int MODE>
 __global__ void k_cta_reduce(ElemArgs A) {
+  pdl_wait();
   using TR = ModeTraits<MODE>;
   constexpr int NOUT = TR::NOUT;
   const int NP = 8 * A.NT;

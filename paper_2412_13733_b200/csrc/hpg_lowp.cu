@@ -80,6 +80,7 @@ template <int P, int Q, bool APPLY>
 #define HPG_LOWP_MINB_SMALL 7
 #endif
 __global__ void __launch_bounds__(LOWP_TH, P <= 4 ? HPG_LOWP_MINB_SMALL : 1) k_lowp(ElemArgs A, const SmallTables tb) {
+  pdl_wait();
   constexpr int N = P - 1, M = P + 1, NIN = APPLY ? 2 : 1;
   constexpr int SL = NIN * N * N > M * M ? NIN * N * N : M * M;
   // thread-private slices: psi (and x) tiles in (1), then the U tile in (2)
@@ -280,8 +281,8 @@ __global__ void __launch_bounds__(LOWP_TH, P <= 4 ? HPG_LOWP_MINB_SMALL : 1) k_l
 
 template <int P, int Q, bool APPLY>
 int go(const ElemArgs& A, const SmallTables& tb, cudaStream_t s) {
-  k_lowp<P, Q, APPLY><<<(A.N + LOWP_TH - 1) / LOWP_TH, LOWP_TH, 0, s>>>(A, tb);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_lowp<P, Q, APPLY>, dim3((A.N + LOWP_TH - 1) / LOWP_TH), dim3(LOWP_TH), 0, s, A, tb);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_lowp launch", e);
 }
 

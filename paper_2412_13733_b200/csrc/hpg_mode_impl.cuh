@@ -121,13 +121,13 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
       return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_cta cluster launch", e);
     }
   }
-  k_cta<MODE, MAXS, W><<<A.N * A.splits, 32 * W, smem, s>>>(A);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_cta<MODE, MAXS, W>, dim3(A.N * A.splits), dim3(32 * W), smem, s, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_cta launch", e);
   if (A.splits > 1) {
     long long total = (long long)A.N * TR::NOUT * A.n * A.n;
-    k_cta_reduce<MODE><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(A);
-    e = cudaGetLastError();
+    e = launch_pdl(k_cta_reduce<MODE>, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, A);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_cta_reduce launch", e);
   }
   return 0;

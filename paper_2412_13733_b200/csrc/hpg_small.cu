@@ -9,8 +9,8 @@ template <int N, int Q, bool RES, bool APPLY>
 int go(const ElemArgs& A, const SmallTables& tb, cudaStream_t s) {
   constexpr int TH = small_threads<N, APPLY>();
   const int grid = (A.N + TH - 1) / TH;
-  k_small<N, Q, RES, APPLY><<<grid, TH, 0, s>>>(A, tb);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_small<N, Q, RES, APPLY>, dim3(grid), dim3(TH), 0, s, A, tb);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_small launch", e);
 }
 

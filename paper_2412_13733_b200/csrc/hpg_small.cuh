@@ -33,6 +33,7 @@ __host__ __device__ constexpr int small_threads() {
 
 template <int N, int Q, bool RES, bool APPLY>
 __global__ void __launch_bounds__(small_threads<N, APPLY>()) k_small(ElemArgs A, const SmallTables tb) {
+  pdl_wait();
   constexpr int NIN = APPLY ? 2 : 1;
   constexpr int TH = small_threads<N, APPLY>();
   __shared__ double sC[NIN][N * N][TH];     // thread-private tile slices

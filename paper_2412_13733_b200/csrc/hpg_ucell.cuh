@@ -475,6 +475,7 @@ __device__ __forceinline__ Sp3 k_row(int j, Inv inv_odd) {
 
 template <bool GRADIENT>
 __global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG, int usplit) {
+  pdl_wait();
   // cpb cell groups of TG threads per CTA (small tiles share a CTA); with few
   // large cells (cpb == 1, config 3) usplit CTAs share one cell's entries
   // (each stages the whole tile, then takes every usplit-th block of TG)
@@ -621,6 +622,7 @@ __global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG, 
 // b_u on the hat-involved interior dofs: alpha f_load + the (up to 4) cell
 // contributions, summed in a fixed order.
 static __global__ void k_hat_gather(ElemArgs A) {
+  pdl_wait();
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int nhx = A.ncx - 1, nhy = A.ncy - 1, m = A.m;
   const long long n1 = (long long)nhx * A.niy;

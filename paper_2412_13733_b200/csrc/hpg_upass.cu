@@ -102,6 +102,7 @@ __device__ __forceinline__ void upass_obstacle(const ElemArgs& A, int e, int lan
 
 template <int P, bool G>
 __global__ void __launch_bounds__(32 * UPW, G ? 1 : 8) k_upass(ElemArgs A) {
+  pdl_wait();
   using U = UPass<P>;
   constexpr int M = U::M, LD = U::LD, BUF = M * LD, N = G ? P : P - 1;
   extern __shared__ double smem[];
@@ -231,8 +232,8 @@ int go(const ElemArgs& A, cudaStream_t s) {
     grid_cap = nsm * (occ > 0 ? occ : 1);
   }
   int need = (A.N + UPW - 1) / UPW;
-  k_upass<P, G><<<need < grid_cap ? need : grid_cap, 32 * UPW, smem, s>>>(A);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_upass<P, G>, dim3(need < grid_cap ? need : grid_cap), dim3(32 * UPW), smem, s, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_upass launch", e);
 }
 

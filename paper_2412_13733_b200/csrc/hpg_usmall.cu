@@ -15,6 +15,7 @@ constexpr int USM_TH = 64;
 
 template <int P, bool G>
 __global__ void __launch_bounds__(USM_TH) k_usmall(ElemArgs A) {
+  pdl_wait();
   constexpr int M = P + 1, N = G ? P : P - 1, NC = G ? 2 : 1;
   extern __shared__ double smem[];
   const int tid = threadIdx.x;
@@ -74,8 +75,8 @@ int go(const ElemArgs& A, cudaStream_t s) {
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_usmall)", e);
     init = true;
   }
-  k_usmall<P, G><<<(A.N + USM_TH - 1) / USM_TH, USM_TH, smem, s>>>(A);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_usmall<P, G>, dim3((A.N + USM_TH - 1) / USM_TH), dim3(USM_TH), smem, s, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_usmall launch", e);
 }
 
