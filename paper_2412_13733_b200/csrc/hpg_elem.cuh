@@ -487,16 +487,17 @@ k_cta(ElemArgs A) {
   const double* tS = A.Sf;
   const double* tT = A.Tf;
   if (A.smem_tables) {
+    // bit 0: PK(S), bit 1: PK(T) (config 3 fits only PK(T) next to its tile)
     double* s0 = sR + NOUT * NT * 64;
-    double* s1 = s0 + QT * NP * 8;
+    double* s1 = s0 + ((A.smem_tables & 1) ? QT * NP * 8 : 0);
     for (int i = 2 * threadIdx.x; i < QT * NP * 8; i += 2 * blockDim.x) {
-      cp_async16(s0 + i, A.Sf + i);
-      cp_async16(s1 + i, A.Tf + i);
+      if (A.smem_tables & 1) cp_async16(s0 + i, A.Sf + i);
+      if (A.smem_tables & 2) cp_async16(s1 + i, A.Tf + i);
     }
     cp_async_commit();
     cp_async_wait_all();
-    tS = s0;
-    tT = s1;
+    if (A.smem_tables & 1) tS = s0;
+    if (A.smem_tables & 2) tT = s1;
   }
   const int rt0 = (sp * QT) / A.splits, rt1 = ((sp + 1) * QT) / A.splits;
   const int cx = e / A.ncy, cy = e - cx * A.ncy;
@@ -657,9 +658,19 @@ __global__ void k_cta_reduce(ElemArgs A) {
   t /= A.n;
   int o = t % NOUT;
   int e = (int)(t / NOUT);
+  // all split partials loaded before the (fixed-order) sum
   double y = 0.0;
-  for (int sp = 0; sp < A.splits; ++sp)
-    y += A.partial[(((long long)e * A.splits + sp) * NOUT + o) * NP * NP + a * NP + b];
+  const double* pp = A.partial + ((long long)e * A.splits * NOUT + o) * NP * NP + a * NP + b;
+  const long long stride = (long long)NOUT * NP * NP;
+  int sp = 0;
+  for (; sp + 8 <= A.splits; sp += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = pp[(sp + q) * stride];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y += v[q];
+  }
+  for (; sp < A.splits; ++sp) y += pp[sp * stride];
   const int cx = e / A.ncy, cy = e - cx * A.ncy;
   write_moment<MODE>(A, e, cx, cy, o, a, b, y);
 }

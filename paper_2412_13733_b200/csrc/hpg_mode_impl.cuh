@@ -64,8 +64,17 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
                                   (size_t)(TR::NSYN * A.NT + TR::NOUT * A.QT + TR::NOUT * A.NT) * 64);
   // stage the tables too when the CTA still fits twice per SM
   const size_t tsmem = sizeof(double) * (size_t)2 * (8 * A.QT) * NP;
-  A.smem_tables = (smem + tsmem) <= 100 * 1024 && getenv("HPG_NO_SMEM_TABLES") == nullptr;
-  if (A.smem_tables) smem += tsmem;
+  // (one CTA per SM when splitting few cells: then PK(T) alone still fits)
+  A.smem_tables = 0;
+  if (getenv("HPG_NO_SMEM_TABLES") == nullptr) {
+    if (smem + tsmem <= 100 * 1024) {
+      A.smem_tables = 3;
+      smem += tsmem;
+    } else if (A.splits > 1 && smem + tsmem / 2 <= 200 * 1024) {
+      A.smem_tables = 2;
+      smem += tsmem / 2;
+    }
+  }
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "element tile too large for shared memory");
   static int attr = 0;
   if ((int)smem > attr) {
