@@ -95,3 +95,28 @@ def test_host_pipelined_matvec(cfg_name, ncells):
     import torch
     ref2 = d.apply_cached_t(torch.from_numpy(x2).cuda()).cpu().numpy()
     assert np.array_equal(D @ x2, ref2)
+
+
+@pytest.mark.parametrize("cfg_name", ["c4p2", "c4p6"])
+@pytest.mark.parametrize("bad", [np.nan, -800.0])
+def test_lowp_flag_and_nan_semantics(cfg_name, bad):
+    """Single-pass kernel vs three-kernel path on a psi with one NaN / one
+    overflowing coefficient: same clamp flag, same NaN pattern, same finite
+    values (reference semantics: assembly.py:187-192, NaN propagates)."""
+    import torch
+    cfg, d, P, inp, dev = build(cfg_name, ncells=9)
+    psi = inp["psi"].copy()
+    psi[len(psi) // 3] = bad
+    tp = torch.from_numpy(psi).cuda()
+
+    def run():
+        b_u, b_psi, y, flag = d.residual_apply_t(cfg.alphas[0], dev["psi_prev"], dev["u"], tp, dev["x"])
+        return b_u.cpu().numpy(), b_psi.cpu().numpy(), y.cpu().numpy(), int(flag.item())
+
+    one = run()
+    three = _with_env("HPG_LOWP_OFF", run)
+    assert one[3] == three[3] == 1
+    for a, b in zip(one[:3], three[:3]):
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        ok = ~np.isnan(a)
+        assert orc.rel_err(a[ok], b[ok]) < TOL
