@@ -31,7 +31,7 @@ __device__ __forceinline__ void upass_obstacle(const ElemArgs& A, int e, int lan
   // C: local U tile (lane = column)
   if (lane < M) {
     const int iy = u_local_1d(cy, lane, A.ncy, P);
-#pragma unroll 4
+#pragma unroll
     for (int i = 0; i < M; ++i) {
       const int ix = u_local_1d(cx, i, A.ncx, P);
       B0[i * LD + lane] = (ix < 0 || iy < 0) ? 0.0 : __ldg(A.u + (long long)ix * A.niy + iy);
@@ -45,6 +45,7 @@ __device__ __forceinline__ void upass_obstacle(const ElemArgs& A, int e, int lan
   __syncwarp();
   if (lane < N) {
     const double wb = hy * kInvOdd[lane];
+#pragma unroll
     for (int a = 0; a < N; ++a) {
       const long long g = base + (long long)a * A.ld + lane;
       A.out[g] = __ldg(A.phi_mom + g) - ((hx * kInvOdd[a]) * B2[a * LD + lane]) * wb;
@@ -64,6 +65,7 @@ __device__ __forceinline__ void upass_obstacle(const ElemArgs& A, int e, int lan
   __syncwarp();
   // B (psi_prev - psi) -> B1
   if (lane < M) {
+#pragma unroll
     for (int i = 0; i < M; ++i) {
       double g = 0.0;
       if (i < N && lane < N) {
@@ -83,6 +85,7 @@ __device__ __forceinline__ void upass_obstacle(const ElemArgs& A, int e, int lan
   if (lane < M) {
     const int k = lane;
     double* edge = A.edge + (long long)e * (4 * M - 4);
+#pragma unroll
     for (int j = 0; j < M; ++j) {
       const double r = -A.alpha * B2[j * LD + k] + B0[j * LD + k];
       if (j >= 2 && k >= 2) {
