@@ -164,7 +164,7 @@ struct WarpCfg {
 #define HPG_REGX_CACHED 8
 #endif
 #ifndef HPG_SPLIT_R
-#define HPG_SPLIT_R 0
+#define HPG_SPLIT_R 1
 #endif
 #ifndef HPG_SPLIT_V
 #define HPG_SPLIT_V 0
@@ -188,7 +188,10 @@ struct WarpCfg {
   static constexpr int W = PIPE ? 2 : WARP_CTA_WARPS;
   static constexpr int CPW = PIPE ? 2 : 1;
   // 4096 cells (config 1) must fit one wave of 4-warp CTAs: >= 7 CTAs / SM
-  static constexpr int MINB_ = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? 7 : 1;
+#ifndef HPG_WARP_MINB
+#define HPG_WARP_MINB 7
+#endif
+  static constexpr int MINB_ = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? HPG_WARP_MINB : 1;
 #ifndef HPG_UNROLL_RT
 #define HPG_UNROLL_RT 0
 #endif
