@@ -1,3 +1,6 @@
+#!/bin/bash
+# Precise A/B of library builds on the default bench (c1): 10 timed steps,
+# twice per build.  VARIANTS="x y" -> paper_2412_13733_b200/libhpg_b200_<x>.so
 cd $GRAFT_REPO_ROOT
 for v in default ${VARIANTS}; do
   lib=""; [ "$v" != default ] && lib=$PWD/paper_2412_13733_b200/libhpg_b200_$v.so
