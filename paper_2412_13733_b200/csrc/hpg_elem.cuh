@@ -175,7 +175,13 @@ struct WarpCfg {
   static constexpr bool cached = MODE == M_OBST_CACHED || MODE == M_GRAD_CACHED;
   // cached modes: the cell's point weights are copied to shared memory with
   // cp.async when they fit (<= 16 KB per warp), read back by the same lane
-  static constexpr int WDBL = QT * QT * TR::NW * 64;
+  static constexpr int WDBL_CELL = QT * QT * TR::NW * 64;
+  // whole-cell staging while it stays small (QT <= 3: config 1); larger QT
+  // (reference rule, nq = 34: QT = 5) keeps two row tiles in flight instead
+  // (ROLL: row tile rt+2 copied while rt+1 is in use), so the weight slices
+  // do not cap the CTAs per SM
+  static constexpr bool ROLL = cached && QT > 3 && 2 * QT * TR::NW * 64 * 8 <= 16 * 1024;
+  static constexpr int WDBL = ROLL ? 2 * QT * TR::NW * 64 : WDBL_CELL;
   static constexpr bool WSMEM = cached && WDBL * 8 <= 16 * 1024;
   static constexpr bool WRITES_WC = MODE == M_OBST_RES || MODE == M_GRAD_RES;
   // cached small tiles (config 1): 2-warp CTAs, each warp streams CPW = 2
@@ -191,7 +197,11 @@ struct WarpCfg {
 #ifndef HPG_WARP_MINB
 #define HPG_WARP_MINB 7
 #endif
-  static constexpr int MINB_ = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? HPG_WARP_MINB : 1;
+#ifndef HPG_ROLL_MINB
+#define HPG_ROLL_MINB 7
+#endif
+  static constexpr int MINB_ = (NT <= 2 && QT <= 3 && TR::NIN == 1) ? HPG_WARP_MINB
+                               : (ROLL && NT <= 2 ? HPG_ROLL_MINB : 1);
 #ifndef HPG_UNROLL_RT
 #define HPG_UNROLL_RT 0
 #endif
@@ -239,8 +249,19 @@ k_warp(ElemArgs A) {
   // weight cache triggers its dependents early (the residual modes below), so
   // a weight cache is always complete when a kernel reading it is launched.
   int buf = 0;
+  // ROLL: one row tile's weights into half h of the warp's slice
+  auto load_rt = [&](int e, int rt, int h) {
+    const double* src = A.wc_in + wc_index(e, QT, rt, 0, NW, 0, lane);
+    double* dst = sW + h * (QT * NW * 64);
+#pragma unroll
+    for (int t = 0; t < QT * NW; ++t) cp_async16(dst + t * 64 + 2 * lane, src + t * 64);
+    cp_async_commit();
+  };
   auto load_weights = [&](int e, int b) {
-    if constexpr (WSMEM) {
+    if constexpr (CF::ROLL) {
+      load_rt(e, 0, 0);
+      load_rt(e, 1, 1);
+    } else if constexpr (WSMEM) {
       const double* src = A.wc_in + wc_index(e, QT, 0, 0, NW, 0, lane);
       double* dst = sW + b * WDBL;
 #pragma unroll
@@ -376,14 +397,21 @@ k_warp(ElemArgs A) {
         for (int f = 0; f < NSYN; ++f) { Vp[f][0] = V[f][ht][0]; Vp[f][1] = V[f][ht][1]; }
         double out2[NOUT][2];
         if constexpr (WSMEM) {
-          if (rt == 0 && ht == 0) {
+          if constexpr (CF::ROLL) {
+            if (ht == 0) {
+              if (rt + 1 < QT) cp_async_wait_group<1>();   // rt in, rt+1 may fly
+              else cp_async_wait_all();
+            }
+          } else if (rt == 0 && ht == 0) {
             if (more) cp_async_wait_group<1>();
             else cp_async_wait_all();
           }
           double Wc[NW][2];
+          const double* wsrc = CF::ROLL ? sW + (rt & 1) * (QT * NW * 64) + (ht * NW) * 64
+                                        : sWc + ((rt * QT + ht) * NW) * 64;
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            const double2 t = *reinterpret_cast<const double2*>(sWc + ((rt * QT + ht) * NW + w) * 64 + 2 * lane);
+            const double2 t = *reinterpret_cast<const double2*>(wsrc + w * 64 + 2 * lane);
             Wc[w][0] = t.x;
             Wc[w][1] = t.y;
           }
@@ -393,6 +421,10 @@ k_warp(ElemArgs A) {
         }
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) { Vw[o][ht][0] = out2[o][0]; Vw[o][ht][1] = out2[o][1]; }
+      }
+      if constexpr (CF::ROLL) {
+        // row tile rt's weights are consumed: its half takes rt + 2
+        if (rt + 2 < QT) load_rt(e, rt + 2, rt & 1);
       }
 #pragma unroll
       for (int o = 0; o < NOUT; ++o) {
