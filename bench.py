@@ -183,7 +183,7 @@ def config_dict(cfg, rule):
 
 # dram bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (cold caches: ncu flushes L2 between replays), see profiles/
-NCU_TRAFFIC = {("c1", "gauss"): (26274816.0 + 256.0, "profiles/r01d_ncu_full_c1_apply.txt"),
+NCU_TRAFFIC = {("c1", "gauss"): (26275072.0, "profiles/r01e_ncu_full_c1_apply.txt"),
                ("c4p6", "gauss"): (90302464.0 + 22354176.0, "profiles/r01b_ncu_full_c4p6_lowp.txt")}
 
 
