@@ -190,6 +190,13 @@ NCU_TRAFFIC = {("c1", "gauss"): (26275072.0, "profiles/r01e_ncu_full_c1_apply.tx
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
+    # torchrun pins OMP_NUM_THREADS=1 per worker; rank 0 alone does the CPU
+    # work here, so give its BLAS / OpenMP pools every host core back
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:
+        pass
     rule = args.rule
     for _ in range(args.warmup):
         cpu_reference_step(cfg, rule)
@@ -336,6 +343,10 @@ def main():
     import torch.distributed as dist
 
     from paper_2412_13733_b200 import dist as hdist
+    if world > 1:
+        # torchrun pins one intra-op thread per worker; the e2e host staging
+        # copies use a fair share of the host cores instead
+        torch.set_num_threads(max(1, (os.cpu_count() or 1) // world))
     torch.cuda.set_device(local)
     hdist.init("nccl")   # one process per GPU; weak scaling: each rank owns a config-sized slab
     from paper_2412_13733_b200 import disc as D
