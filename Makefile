@@ -17,7 +17,7 @@ $(OBJDIR)/%.o: $(CS)/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
 
 $(PKG)/libhpg_b200.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcublas
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 clean:
 	rm -rf $(OBJDIR) $(PKG)/libhpg_b200.so

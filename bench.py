@@ -1,26 +1,40 @@
 #!/usr/bin/env python
 """Benchmark: fp64 element-quadrature-points/s for residual + Jacobian apply.
 
-Metric (BASELINE.json): EQP/s = N * Q^2 * (1 + k_mv) / t for
-one "step" = 1 LVPP residual (proximal.residual: b_u, b_psi, clamp flag) +
-k_mv Jacobian matvecs D(psi) x, on synthetic seeded inputs with the config's
-shapes (no public dataset exists for this path).  Default workload: config 1
-(64x64 mesh, p=16, Q=24 Gauss, 1 residual + 50 matvecs, alpha cycling over
-{1, 4, 16}) -- the largest single-GPU configuration BASELINE.json quotes.
+Metric (BASELINE.json): EQP/s = N * Q^2 * (1 + k_mv) * reps / t
+for one "step" = 1 LVPP residual (proximal.residual: b_u, b_psi, clamp flag) +
+k_mv Jacobian matvecs D(psi) x (x reps for config 4), on synthetic seeded
+inputs with the config's shapes (no public dataset exists for this path).
+Headline workload (the JSON line's top-level fields): config 1 (64x64 mesh,
+p=16, Q=24 Gauss, 1 residual + 50 matvecs, alpha cycling over {1, 4, 16}) --
+the largest single-GPU configuration BASELINE.json quotes.  ``per_config``
+carries the same measurement for all five BASELINE configs (c4 at p = 2, 4, 6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
 
-Prints ONE JSON line on rank 0.  ``value`` is device-timed (CUDA events on the
-launching stream, inputs resident in HBM, L2 flushed between timed steps);
-``e2e`` is the same metric through the reference-facing NumPy API with host
-buffers (H2D/D2H inside the timed region).
+Prints ONE JSON line on rank 0.
+* ``value``: device-timed (CUDA events on the launching stream, inputs
+  resident in HBM).  L2: flushed between timed steps (256 MB write); config 4
+  additionally rotates its 100 repetitions over >= 3 input/output buffer sets
+  totalling more than twice the 126 MB L2, so every repetition streams HBM;
+  the Krylov matvecs of the cached configs rotate over 8 direction vectors
+  (the weight cache of D(psi) is shared by all matvecs of a Newton step, as
+  in GMRES).
+* ``e2e``: the same metric through the reference-facing NumPy API with host
+  buffers (H2D / D2H inside the timed region).
+* ``cpu_baseline`` / ``--impl reference``: the UNMODIFIED reference package
+  (hpgalerkin, installed into oracle/_ref by oracle/build_ref.sh) timed on the
+  box's host cores on a bounded sample of the same workload: its own
+  ``exp_moments`` / ``nl_moments`` + k_mv ``apply_D`` per repetition
+  ("hot-only", the line's value) and ``proximal.residual`` as-is.
 """
 
 import argparse
 import json
+import math
 import os
+import platform
 import statistics
-import subprocess
 import sys
 import time
 
@@ -34,17 +48,20 @@ from paper_2412_13733_b200.workloads import CONFIGS, config_inputs  # noqa: E402
 METRIC = "fp64 element-quadrature-points/sec for residual+Jacobian apply"
 UNIT = "EQP/s"
 P_FP64_TFLOPS = 37.17       # measured DMMA peak, profiles/fp64_peaks_r01.json
+L2_BYTES = 126 << 20
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+ALL = ("c0", "c1", "c2", "c3", "c4p2", "c4p4", "c4p6")
+# cells per direction of the reference's bounded CPU sample (its per-cell cost
+# is mesh-size independent: a Python loop over cells)
+REF_SAMPLE_CELLS = {"c0": 4, "c1": 16, "c2": 4, "c3": 1, "c4p2": 16, "c4p4": 16, "c4p6": 16}
 
 
 def peaks():
-    hbm = None
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            hbm = float(json.load(f)["hbm_gbs"])
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     except Exception:
-        hbm = 6650.0
-    return hbm
+        return 6650.0, "fallback (no MEASURED_PEAKS.json)"
 
 
 def syn_flops(n, Q):
@@ -65,8 +82,7 @@ def algorithmic(cfg, disc_n, nq, ndof_psi, ndof_u):
 
 class ClockSampler:
     """SM clock + clock-event (throttle) reasons sampled DURING the timed region
-    through NVML (nvidia-ml-py) every ~2 ms in a background thread; falls back
-    to `nvidia-smi -lms 100` when NVML is unavailable."""
+    through NVML (nvidia-ml-py) every ~2 ms in a background thread."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
@@ -116,55 +132,151 @@ class ClockSampler:
                 "source": "NVML during the timed region"}
 
 
-def cpu_reference_step(cfg, rule, cells_frac=None):
-    """One bounded sample of the workload on the CPU oracle (numpy port of the
-    reference's per-cell algorithm, oracle/hpg_oracle.py).  Returns
-    (seconds, eqp_in_sample, sample description)."""
-    from types import SimpleNamespace
+# ---------------------------------------------------------------------------
+# the reference (CPU) arm: the unmodified hpgalerkin package
 
-    from oracle import hpg_oracle as orc
-    from paper_2412_13733_b200.tables import Tables
-    nc_full = cfg.ncells
-    # bound the sample: at most ~4096 cells x 8 matvecs of c1 size
-    ncells = nc_full
-    kmv = cfg.k_mv
-    if cfg.name == "c1":
-        kmv = 5
-    if cfg.name.startswith("c4"):
-        ncells = 64
-    t = Tables(rule, cfg.p, cfg.n, cfg.nq(rule))
-    tt = SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq)
-    x = np.linspace(0.0, 1.0, ncells + 1)
-    P = orc.Problem(cfg.kind, x, x, cfg.p, tt)
-    inp = config_inputs(cfg, ncells=ncells)
-    phi_vals = P.sample(inp["phi"])
-    f_load = P.load_vector(P.sample(1.0))
-    if cfg.kind == "obstacle":
-        phi_mom = P.data_moments(phi_vals)
-    t0 = time.perf_counter()
-    if cfg.kind == "obstacle":
-        P.residual(cfg.alphas[0], inp["psi_prev"], inp["u"], inp["psi"], f_load, phi_moments=phi_mom)
-        for _ in range(kmv):
-            P.obstacle_apply_D(inp["psi"], inp["x"])
-    else:
-        P.residual(cfg.alphas[0], inp["psi_prev"], inp["u"], inp["psi"], f_load, phi_vals=phi_vals)
-        for _ in range(kmv):
-            P.gradient_apply_D(inp["psi"], inp["x"], phi_vals)
-    dt = time.perf_counter() - t0
-    eqp = ncells * ncells * t.nq ** 2 * (1 + kmv)
-    desc = (f"oracle (numpy port of hpgalerkin per-cell quadrature, batched over cells) on "
-            f"{ncells}x{ncells} cells of {cfg.name} (p={cfg.p}, {rule} rule nq={t.nq}): "
-            f"1 residual + {kmv} apply_D")
-    return dt, eqp, desc
-
-
-def cpu_threads():
+def cpu_model():
     try:
-        from threadpoolctl import threadpool_info
-        info = threadpool_info()
-        return max([i.get("num_threads", 1) for i in info] + [1])
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
     except Exception:
-        return os.cpu_count() or 1
+        pass
+    return platform.processor() or "unknown"
+
+
+def _reference():
+    """hpgalerkin from oracle/_ref (oracle/build_ref.sh); raises when missing."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "hpgalerkin")) and ref not in sys.path:
+        sys.path.append(ref)
+    import hpgalerkin.assembly  # noqa: F401
+    import hpgalerkin.proximal  # noqa: F401
+    return sys.modules["hpgalerkin"]
+
+
+class ReferenceSample:
+    """The reference's own disc on a cfg-degree mesh of ``nc`` x ``nc`` cells;
+    rule='gauss' substitutes the Gauss tables into its CellKernel1D objects
+     and refreshes its data terms."""
+
+    def __init__(self, cfg, rule, nc):
+        hp = _reference()
+        from hpgalerkin import assembly as ra
+        from hpgalerkin.mesh import uniform_mesh_2d
+
+        from paper_2412_13733_b200.tables import Tables
+        self.cfg, self.rule, self.nc = cfg, rule, nc
+        inp = config_inputs(cfg, ncells=nc)
+        mesh = uniform_mesh_2d(0.0, 1.0, nc, cfg.p)
+        cls = ra.ObstacleDisc2D if cfg.kind == "obstacle" else ra.GradientDisc2D
+        d = cls(mesh, inp["f"], inp["phi"])
+        t = Tables(rule, cfg.p, cfg.n, cfg.nq(rule))
+        if rule == "gauss":
+            for k2 in d.kernels.values():
+                for k1 in (k2.kx, k2.ky):
+                    k1.nquad = t.nq
+                    k1.points = k1.midpoint + 0.5 * k1.h * t.xi
+                    k1.S, k1.T, k1.Su, k1.Tu = t.S, t.T, t.Su, t.Tu
+            d.f_load = d.load_vector(inp["f"])
+            if cfg.kind == "obstacle":
+                d.phi_moments = d.data_moments(inp["phi"])
+            else:
+                d.phi_values = {c: ra._eval_data(inp["phi"], d.kernels[c], "pointwise", 2) for c in d.cell_ids}
+        self.disc, self.inp, self.nq = d, inp, t.nq
+        self.hp = hp
+        self.eqp_rep = nc * nc * t.nq ** 2 * (1 + cfg.k_mv)
+
+    def run(self):
+        """One repetition: returns (t_hot, t_as_is) in seconds.
+        hot-only = exp/nl_moments + k_mv apply_D; as-is = proximal.residual + k_mv apply_D."""
+        from hpgalerkin import proximal
+        d, inp, k = self.disc, self.inp, self.cfg.k_mv
+        t0 = time.perf_counter()
+        if self.cfg.kind == "obstacle":
+            d.exp_moments(inp["psi"])
+        else:
+            d.nl_moments(inp["psi"])
+        t1 = time.perf_counter()
+        for _ in range(k):
+            d.apply_D(inp["psi"], inp["x"])
+        t2 = time.perf_counter()
+        proximal.residual(d, self.cfg.alphas[0], inp["psi_prev"], inp["u"], inp["psi"])
+        t3 = time.perf_counter()
+        return (t1 - t0) + (t2 - t1), (t3 - t2) + (t2 - t1)
+
+    def describe(self):
+        c = self.cfg
+        return (f"unmodified hpgalerkin {getattr(self.hp, '__version__', '?')} (oracle/_ref) on a "
+                f"{self.nc}x{self.nc}-cell mesh of {c.name}'s degree (p={c.p}, {self.rule} rule "
+                f"nq={self.nq}): per repetition exp/nl_moments + {c.k_mv} apply_D (hot-only; "
+                f"as-is: proximal.residual + {c.k_mv} apply_D)")
+
+
+def _threads(n):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
+    except Exception:
+        class _Nop:
+            def __enter__(self):
+                return self
+
+            def __exit__(self, *a):
+                return False
+        return _Nop()
+
+
+def reference_baseline(cfg, rule, reps=2, one_thread=True):
+    """cpu_baseline record: the reference on all host cores (and on 1)."""
+    cores = os.cpu_count() or 1
+    s = ReferenceSample(cfg, rule, REF_SAMPLE_CELLS[cfg.name])
+    with _threads(cores):
+        s.run()                                   # warm-up
+        hot, asis = zip(*[s.run() for _ in range(reps)])
+    rec = {"value": s.eqp_rep / min(hot), "unit": UNIT, "cores": cores, "kind": "reference",
+           "cpu_model": cpu_model(), "sample": s.describe() + f"; best of {reps}",
+           "as_is_value": s.eqp_rep / min(asis)}
+    if one_thread:
+        with _threads(1):
+            hot1 = min(s.run()[0] for _ in range(reps))
+        rec["value_1thread"] = s.eqp_rep / hot1
+    return rec
+
+
+def run_reference(args, cfg, rank, world):
+    """``--impl reference``: the unmodified reference on the host cores
+    (rank 0 alone; the other ranks exit without work)."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    rule = args.rule
+    s = ReferenceSample(cfg, rule, REF_SAMPLE_CELLS[cfg.name])
+    with _threads(cores):
+        for _ in range(args.warmup):
+            s.run()
+        times, asis = [], []
+        for _ in range(args.steps):
+            th, ta = s.run()
+            times.append(th)
+            asis.append(ta)
+        with _threads(1):
+            t1 = s.run()[0]
+    value = s.eqp_rep * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8d)",
+        "config": config_dict(cfg, rule),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "cpu_model": cpu_model(), "sample": s.describe(),
+                         "as_is_value": s.eqp_rep * len(asis) / sum(asis),
+                         "value_1thread": s.eqp_rep / t1},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def config_dict(cfg, rule):
@@ -177,7 +289,9 @@ def config_dict(cfg, rule):
                         + (f", alpha cycling {list(cfg.alphas)}" if len(cfg.alphas) > 1 else ""),
             "rule": rule, "ncells": cfg.N, "p": cfg.p, "nq": nq, "k_mv": cfg.k_mv, "reps": cfg.reps,
             "matvec": "cached point weights" if cached else "weights recomputed from psi (fused with the residual)",
-            "l2": "flushed between timed steps (256 MB write)",
+            "l2": ("flushed between timed steps (256 MB write); repetitions rotate over buffer sets "
+                   "> 2x L2" if not cached else "flushed between timed steps (256 MB write); matvecs "
+                   "rotate over 8 direction vectors"),
             "eqp_per_step": cfg.N * nq * nq * (1 + cfg.k_mv) * cfg.reps}
 
 
@@ -187,39 +301,8 @@ NCU_TRAFFIC = {("c1", "gauss"): (26275072.0, "profiles/r01e_ncu_full_c1_apply.tx
                ("c4p6", "gauss"): (90302464.0 + 22354176.0, "profiles/r01b_ncu_full_c4p6_lowp.txt")}
 
 
-def run_reference(args, cfg, rank, world):
-    if rank != 0:
-        return
-    # torchrun pins OMP_NUM_THREADS=1 per worker; rank 0 alone does the CPU
-    # work here, so give its BLAS / OpenMP pools every host core back
-    try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(limits=os.cpu_count() or 1)
-    except Exception:
-        pass
-    rule = args.rule
-    for _ in range(args.warmup):
-        cpu_reference_step(cfg, rule)
-    times, eqps = [], []
-    desc = ""
-    for _ in range(args.steps):
-        dt, eqp, desc = cpu_reference_step(cfg, rule)
-        times.append(dt)
-        eqps.append(eqp)
-    value = sum(eqps) / sum(times)
-    cores = cpu_threads()
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, SURVEY.md §8d)",
-        "config": config_dict(cfg, rule),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": desc},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
+# ---------------------------------------------------------------------------
+# the B200 arm
 
 def precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm):
     """Factor (P blocks + LU) and apply (per-cell solves) of the device
@@ -258,7 +341,8 @@ def precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm):
 
 def schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag):
     """Stiffness solve (fast diagonalisation), one-call Schur apply and one
-    full schur_solve (device preconditioner, GMRES rtol 1e-8) at beta = 1e-8."""
+    full schur_solve (device preconditioner, device GMRES graph, rtol 1e-8) at
+    beta = 1e-8."""
     import torch
     from paper_2412_13733_b200 import schur
     alpha, beta = cfg.alphas[-1], 1e-8
@@ -267,6 +351,7 @@ def schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag):
     D = disc.assemble_D_t(psi)
     S = schur.DeviceSchurOperator(disc, D, beta, alpha, Af)
     M = disc.schur_preconditioner(D, alpha, beta)
+    G = schur.DeviceGmres(disc.ndof_psi, 150, disc.device)
     xs = torch.empty_like(u)
     ys = torch.empty_like(psi)
     out = {}
@@ -286,7 +371,7 @@ def schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag):
     t_apply = timed(lambda: S.matvec_t(psi, out=ys), 10)
 
     def full():
-        out["r"] = schur.schur_solve_t(disc, D, alpha, beta, bu, bp, Af, rtol=1e-8, precond=M)
+        out["r"] = schur.schur_solve_t(disc, D, alpha, beta, bu, bp, Af, rtol=1e-8, precond=M, gmres=G)
 
     t_full = timed(full, 2)
     nix = cfg.ncells * cfg.p - 1
@@ -294,27 +379,227 @@ def schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag):
     return {"beta": beta, "stiffness_solve_us": t_solve * 1e6, "stiffness_solve_tflops": fl / t_solve / 1e12,
             "schur_apply_us": t_apply * 1e6, "schur_solve_ms": t_full * 1e3,
             "gmres_iterations": out["r"].gmres.iterations,
-            "path": "hpgStiffnessSolve (fast diagonalisation, cuBLAS DGEMM), hpgSchurApply, "
-                    "schur.schur_solve_t (device GMRES + hpgLUSolve), preconditioner factor excluded"}
+            "path": "hpgStiffnessSolve (fast diagonalisation, own DMMA GEMMs), hpgSchurApply, "
+                    "schur.schur_solve_t (device GMRES graph + hpgLUSolve), preconditioner factor excluded"}
 
 
-def solve_timing(disc):
-    """proximal.solve from zero with AlphaSchedule(1, 2, alpha_max=16), beta = 1e-8:
-    wall time (synchronised) including the one-time stiffness eigen-factorisation."""
+def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
+    """Device-timed measurement of one config; ``full`` adds the headline-only
+    extras (preconditioner, Schur solve)."""
     import torch
-    from paper_2412_13733_b200 import proximal
-    proximal.solve(disc, proximal.AlphaSchedule(alpha0=1.0, nsteps=1), 1e-8)     # warm-up
+
+    from paper_2412_13733_b200 import _lib
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200 import dist as hdist
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    from paper_2412_13733_b200.proximal import residual
+
+    nq = cfg.nq(rule)
+    inp = config_inputs(cfg, seed=0)
+    mesh = uniform_mesh_2d(0.0, 1.0, cfg.ncells, cfg.p)
+    cls = D.ObstacleDisc2D if cfg.kind == "obstacle" else D.GradientDisc2D
+    disc = cls(mesh, inp["f"], inp["phi"], rule=rule, nq=nq if rule == "gauss" else None)
+    dev = disc.device
+    cached = not cfg.name.startswith("c4")
+    kmv, reps = cfg.k_mv, cfg.reps
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def new_set():
+        return {"psi": t(inp["psi"]), "psi_prev": t(inp["psi_prev"]), "u": t(inp["u"]), "x": t(inp["x"]),
+                "b_u": torch.empty(disc.ndof_u, dtype=torch.float64, device=dev),
+                "b_psi": torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev),
+                "y": torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev)}
+
+    set_bytes = 8 * (5 * disc.ndof_psi + 2 * disc.ndof_u)
+    nsets = max(3, math.ceil(2 * L2_BYTES / set_bytes)) if not cached else 1
+    sets = [new_set() for _ in range(nsets)]
+    s0 = sets[0]
+    NX = 8
+    xs = [s0["x"]] + [s0["x"].clone() for _ in range(NX - 1)] if cached else None
+    ys = [torch.empty_like(s0["y"]) for _ in range(NX)] if cached else None
+
+    def step_residual(alpha):
+        if cached:
+            disc.residual_t(alpha, s0["psi_prev"], s0["u"], s0["psi"], b_u=s0["b_u"], b_psi=s0["b_psi"],
+                            flag=flag, wcache=True)
+        else:
+            for r in range(reps):
+                st = sets[r % nsets]
+                disc.residual_apply_t(alpha, st["psi_prev"], st["u"], st["psi"], st["x"], b_u=st["b_u"],
+                                      b_psi=st["b_psi"], y=st["y"], flag=flag)
+
+    def step_matvecs(k):
+        for i in range(k):
+            disc.apply_cached_t(xs[i % NX], out=ys[i % NX])
+
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        for a in cfg.alphas:
+            step_residual(a)
+        if cached:
+            step_matvecs(kmv)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    rep = proximal.solve(disc, proximal.AlphaSchedule(alpha0=1.0, rate=2.0, alpha_max=16.0), 1e-8)
+    g_res = {}
+    for a in cfg.alphas:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step_residual(a)
+        g_res[a] = g
+    g_mv = g_kern = None
+    KREP = 20
+    if cached:
+        g_mv = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_mv, stream=stream):
+            step_matvecs(kmv)
+        g_kern = torch.cuda.CUDAGraph()                 # dominant-kernel timing replay
+        with torch.cuda.graph(g_kern, stream=stream):
+            step_matvecs(KREP)
     torch.cuda.synchronize()
-    t = time.perf_counter() - t0
-    return {"seconds": t, "converged": rep.converged, "alphas": [s.alpha for s in rep.steps],
-            "newton_per_step": [s.newton_iters for s in rep.steps],
-            "gmres_per_step": [s.gmres_total for s in rep.steps],
-            "ms_per_newton_step": t / max(1, rep.newton_total) * 1e3,
-            "t_assembly_s": rep.t_assembly_s, "t_linsolve_s": rep.t_linsolve_s,
-            "path": "paper_2412_13733_b200.proximal.solve (device Newton + Schur GMRES)"}
+
+    launches_per_residual = 3 + (1 if disc.plan.splits > 1 and disc.plan.path == 1 else 0)
+    launches_per_step = (launches_per_residual + kmv) if cached else disc.plan.residual_apply_kernels * reps
+
+    def run_steps(nsteps):
+        evs = []
+        for s in range(nsteps):
+            a = cfg.alphas[s % len(cfg.alphas)]
+            flush.fill_(float(s))                  # evict L2 between steps
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            g_res[a].replay()
+            e1.record(stream)
+            if g_mv is not None:
+                g_mv.replay()
+            e2.record(stream)
+            evs.append((e0, e1, e2))
+        return evs
+
+    with torch.cuda.stream(stream):
+        run_steps(args.warmup)
+        torch.cuda.synchronize()
+        hdist.barrier(dev)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            evs = run_steps(args.steps)
+            torch.cuda.synchronize()
+        hdist.barrier(dev)
+        torch.cuda.synchronize()
+        t_kern = None
+        if g_kern is not None:
+            g_kern.replay()
+            torch.cuda.synchronize()
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record(stream)
+            for _ in range(3):
+                g_kern.replay()
+            k1.record(stream)
+            torch.cuda.synchronize()
+            t_kern = k0.elapsed_time(k1) * 1e-3 / (3 * KREP)
+    step_ms = [e0.elapsed_time(e2) for e0, e1, e2 in evs]
+    res_ms = [e0.elapsed_time(e1) for e0, e1, e2 in evs]
+    mv_ms = [e1.elapsed_time(e2) for e0, e1, e2 in evs] if cached else None
+    total_ms = hdist.max_over_ranks(sum(step_ms), dev)       # slowest rank
+    eqp_step = cfg.N * nq * nq * (1 + kmv) * reps
+    value = hdist.aggregate_throughput(eqp_step, args.steps, world, total_ms * 1e-3)
+
+    F_res, F_mv, B_res, B_mv = algorithmic(cfg, disc.n, nq, disc.ndof_psi, disc.ndof_u)
+    hbm, hbm_src = peaks()
+    traffic, traffic_src = NCU_TRAFFIC.get((cfg.name, rule), (None, "not captured for this config"))
+    if cached:
+        achieved = F_mv / t_kern / 1e12
+        roof = {"kernel": ("k_warp<NT,QT,M_OBST_CACHED>" if disc.plan.path == 0 else "k_cta<M_*_CACHED>")
+                          + " (Jacobian apply from cached weights)",
+                "bound": "tensor", "achieved": achieved, "peak": P_FP64_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / P_FP64_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peaks_r01.json)",
+                "algorithmic_per_launch": {"flops": F_mv, "bytes": B_mv},
+                "avg_launch_us": t_kern * 1e6,
+                "timing": f"CUDA events around {KREP} back-to-back launches (graph) on the launching stream"}
+    else:
+        t_k = statistics.mean(res_ms) / reps * 1e-3       # fused residual + apply per rep
+        bytes_ = B_res + B_mv
+        achieved = bytes_ / t_k / 1e9
+        roof = {"kernel": "k_lowp<p,Q,apply> (single-pass residual + Jacobian apply, one launch per rep)",
+                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": hbm_src,
+                "algorithmic_per_launch": {"flops": F_res + F_mv, "bytes": bytes_},
+                "avg_launch_us": t_k * 1e6,
+                "timing": f"CUDA events around the step's {reps} launches (buffer sets rotated: {nsets})"}
+    t_lb = max((F_res + kmv * F_mv) / (P_FP64_TFLOPS * 1e12), (B_res + kmv * B_mv) / (hbm * 1e9)) * reps
+    step_frac = t_lb / (statistics.mean(step_ms) * 1e-3)
+
+    # e2e through the reference-facing NumPy API (host buffers)
+    e2e = None
+    if e2e_steps > 0:
+        hp = {k: np.ascontiguousarray(inp[k]) for k in ("psi", "psi_prev", "u", "x")}
+        torch.cuda.synchronize()
+        t_e2e = []
+        for s in range(e2e_steps + 1):
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                residual(disc, cfg.alphas[s % len(cfg.alphas)], hp["psi_prev"], hp["u"], hp["psi"])
+                Dm = disc.assemble_D(hp["psi"]) if cached else None
+                for _ in range(kmv):
+                    (Dm @ hp["x"]) if cached else disc.apply_D(hp["psi"], hp["x"])
+            torch.cuda.synchronize()
+            if s > 0:
+                t_e2e.append(time.perf_counter() - t0)
+        h2d = 8 * reps * (2 * disc.ndof_psi + disc.ndof_u + (disc.ndof_psi if cached else 0)
+                          + kmv * disc.ndof_psi * (1 if cached else 2))
+        d2h = 8 * reps * (disc.ndof_u + disc.ndof_psi + kmv * disc.ndof_psi) + 4 * reps
+        e2e_s = hdist.max_over_ranks(statistics.mean(t_e2e), dev)
+        e2e = {"value": eqp_step * world / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": 1e3 * e2e_s,
+               "ms_per_step_min_median_max": [1e3 * min(t_e2e), 1e3 * statistics.median(t_e2e), 1e3 * max(t_e2e)],
+               "path": "paper_2412_13733_b200.proximal.residual + disc.assemble_D + (D @ x) x k_mv, NumPy in/out"}
+
+    rec = {"config": config_dict(cfg, rule), "value": value, "ms_per_step": total_ms / args.steps,
+           "roofline": roof, "step_roofline_frac": step_frac, "e2e": e2e,
+           "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+           "res_ms_mean": statistics.mean(res_ms), "mv_ms_mean": statistics.mean(mv_ms) if mv_ms else None,
+           "buffer_sets": nsets}
+
+    # element-block assembly (reported separately, SURVEY.md §8d): configs whose
+    # BASELINE workload includes it
+    if cfg.name in ("c0", "c2", "c3") and world == 1:
+        disc.residual_t(cfg.alphas[0], s0["psi_prev"], s0["u"], s0["psi"], b_u=s0["b_u"], b_psi=s0["b_psi"],
+                        flag=flag, wcache=True)
+        nbl = disc.plan.block_len
+        out_blk = torch.empty((cfg.N, nbl), dtype=torch.float64, device=dev)
+        disc.blocks_t(out=out_blk)
+        torch.cuda.synchronize()
+        eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eb0.record()
+        disc.blocks_t(out=out_blk)
+        eb1.record()
+        torch.cuda.synchronize()
+        t_blk = eb0.elapsed_time(eb1) * 1e-3
+        nb_ = cfg.ncomp * disc.n * disc.n
+        nbfield = 1 if cfg.kind == "obstacle" else 3
+        F_blk = cfg.N * nbfield * (2.0 * disc.n ** 4 * nq + 2.0 * disc.n ** 2 * nq ** 2)
+        B_blk = 8.0 * cfg.N * nb_ * nb_ + 8.0 * disc.ndof_psi
+        lb = max(F_blk / (P_FP64_TFLOPS * 1e12), B_blk / (hbm * 1e9))
+        rec["blocks"] = {"ms": t_blk * 1e3, "tflops": F_blk / t_blk / 1e12, "gbs": B_blk / t_blk / 1e9,
+                         "roofline_frac": lb / t_blk, "bytes": B_blk, "flops": F_blk}
+        del out_blk
+    if full and world == 1:
+        lu_fits = cfg.ncomp * disc.n * disc.n <= _lib.load().hpgLUMaxBlock()
+        if lu_fits:
+            rec["precond"] = precond_timing(disc, cfg, s0["psi_prev"], s0["u"], s0["psi"], s0["x"],
+                                            s0["b_u"], s0["b_psi"], flag, hbm)
+        if disc.plan.ndof_u > 0:
+            rec["schur"] = (schur_timing(disc, cfg, s0["psi_prev"], s0["u"], s0["psi"], s0["b_u"],
+                                         s0["b_psi"], flag) if lu_fits else
+                            {"unsupported": "per-cell LU block side exceeds hpgLUMaxBlock()"})
+    del sets, g_res, g_mv, g_kern
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return rec
 
 
 def main():
@@ -327,6 +612,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--only", action="store_true", help="measure the headline config alone (no per_config)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -334,8 +620,6 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        # the reference arm is a CPU run: rank 0 alone measures and prints, the
-        # other ranks exit without work
         run_reference(args, cfg, rank, world)
         return
 
@@ -348,240 +632,61 @@ def main():
         # copies use a fair share of the host cores instead
         torch.set_num_threads(max(1, (os.cpu_count() or 1) // world))
     torch.cuda.set_device(local)
-    hdist.init("nccl")   # one process per GPU; weak scaling: each rank owns a config-sized slab
-    from paper_2412_13733_b200 import disc as D
-    from paper_2412_13733_b200.mesh import uniform_mesh_2d
-    from paper_2412_13733_b200.proximal import residual
-
+    hdist.init("nccl")
     rule = args.rule
-    nq = cfg.nq(rule)
-    inp = config_inputs(cfg, seed=rank)       # each rank: its own slab of elements (weak scaling)
-    mesh = uniform_mesh_2d(0.0, 1.0, cfg.ncells, cfg.p)
-    cls = D.ObstacleDisc2D if cfg.kind == "obstacle" else D.GradientDisc2D
-    disc = cls(mesh, inp["f"], inp["phi"], rule=rule, nq=nq if rule == "gauss" else None)
-    dev = disc.device
-    psi = torch.from_numpy(inp["psi"]).to(dev)
-    psi_prev = torch.from_numpy(inp["psi_prev"]).to(dev)
-    u = torch.from_numpy(inp["u"]).to(dev)
-    x = torch.from_numpy(inp["x"]).to(dev)
-    b_u = torch.empty(disc.ndof_u, dtype=torch.float64, device=dev)
-    b_psi = torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev)
-    y = torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    cached = not cfg.name.startswith("c4")      # c4: HBM-bound, recompute weights from psi
-    kmv = cfg.k_mv
-    reps = cfg.reps
-
-    def step_residual(alpha):
-        if cached:
-            # residual + the point weights of D(psi) for the Krylov matvecs
-            disc.residual_t(alpha, psi_prev, u, psi, b_u=b_u, b_psi=b_psi, flag=flag, wcache=True)
-        else:
-            # residual + Jacobian apply at the same psi in one pass (hpgResidualApply)
-            disc.residual_apply_t(alpha, psi_prev, u, psi, x, b_u=b_u, b_psi=b_psi, y=y, flag=flag)
-
-    def step_matvecs():
-        for _ in range(kmv):
-            if cached:
-                disc.apply_cached_t(x, out=y)
+    head = gpu_config(cfg, rule, args, local, world, full=True, e2e_steps=args.e2e_steps)
+    per = {}
+    if not args.only:
+        for name in ALL:
+            if name == cfg.name:
+                rec = head
             else:
-                disc.apply_D_t(psi, x, out=y)
-
-    # per-alpha graphs: residual, then matvecs (captured once each)
-    stream = torch.cuda.Stream()
-    stream.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(stream):
-        for a in cfg.alphas:
-            step_residual(a)
-        step_matvecs()
-    torch.cuda.synchronize()
-    g_res = {}
-    for a in cfg.alphas:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for _ in range(reps if not cached else 1):
-                step_residual(a)
-        g_res[a] = g
-    g_mv = None
-    if cached:
-        g_mv = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_mv, stream=stream):
-            step_matvecs()
-    torch.cuda.synchronize()
-
-    launches_per_residual = 3 + (1 if disc.plan.splits > 1 and disc.plan.path == 1 else 0)
-    launches_per_step = (launches_per_residual + kmv) if cached else disc.plan.residual_apply_kernels * reps
-
-    def run_steps(nsteps, timed):
-        evs = []
-        for s in range(nsteps):
-            a = cfg.alphas[s % len(cfg.alphas)]
-            flush.fill_(float(s))                  # evict L2 between steps
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e2 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            g_res[a].replay()
-            e1.record(stream)
-            if g_mv is not None:
-                g_mv.replay()
-            e2.record(stream)
-            evs.append((e0, e1, e2))
-        return evs
-
-    with torch.cuda.stream(stream):
-        run_steps(args.warmup, False)
-        torch.cuda.synchronize()
-        hdist.barrier(dev)
-        torch.cuda.synchronize()
-        with ClockSampler(local) as clk:
-            evs = run_steps(args.steps, True)
-            torch.cuda.synchronize()
-        hdist.barrier(dev)
-        torch.cuda.synchronize()
-    step_ms = [e0.elapsed_time(e2) for e0, e1, e2 in evs]
-    res_ms = [e0.elapsed_time(e1) for e0, e1, e2 in evs]
-    mv_ms = [e1.elapsed_time(e2) for e0, e1, e2 in evs] if cached else None
-    total_ms = hdist.max_over_ranks(sum(step_ms), dev)       # slowest rank
-    eqp_step = cfg.N * nq * nq * (1 + kmv) * reps
-    value = hdist.aggregate_throughput(eqp_step, args.steps, world, total_ms * 1e-3)
-
-    # roofline of the dominant kernel
-    F_res, F_mv, B_res, B_mv = algorithmic(cfg, disc.n, nq, disc.ndof_psi, disc.ndof_u)
-    hbm = peaks()
-    if cached:
-        t_k = statistics.mean(mv_ms) / kmv * 1e-3
-        achieved = F_mv / t_k / 1e12
-        roof = {"kernel": "k_warp<NT,QT,M_OBST_CACHED> (Jacobian apply from cached weights)"
-                if cfg.kind == "obstacle" else "Jacobian apply from cached weights (gradient)",
-                "bound": "tensor", "achieved": achieved, "peak": P_FP64_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / P_FP64_TFLOPS,
-                "traffic": NCU_TRAFFIC.get((cfg.name, rule), (None, None))[0],
-                "traffic_source": NCU_TRAFFIC.get((cfg.name, rule), (None, "not captured for this config"))[1],
-                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peaks_r01.json)",
-                "algorithmic_per_launch": {"flops": F_mv, "bytes": B_mv},
-                "avg_launch_us": t_k * 1e6}
-    else:
-        t_k = statistics.mean(res_ms) / reps * 1e-3       # fused residual + apply per rep
-        bytes_ = B_res + B_mv
-        achieved = bytes_ / t_k / 1e9
-        roof = {"kernel": "k_lowp<p,Q,apply> (single-pass residual + Jacobian apply, one launch per rep)",
-                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm,
-                "traffic": NCU_TRAFFIC.get((cfg.name, rule), (None, None))[0],
-                "traffic_source": NCU_TRAFFIC.get((cfg.name, rule), (None, "not captured for this config"))[1],
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "algorithmic_per_launch": {"flops": F_res + F_mv, "bytes": bytes_},
-                "avg_launch_us": t_k * 1e6}
-    # roofline-combined lower bound for the whole step
-    t_lb = max((F_res + kmv * F_mv) / (P_FP64_TFLOPS * 1e12), (B_res + kmv * B_mv) / (hbm * 1e9)) * reps
-    step_frac = t_lb / (statistics.mean(step_ms) * 1e-3)
-
-    # e2e through the reference-facing NumPy API (host buffers)
-    e2e = None
-    if args.e2e_steps > 0:
-        hp = {k: np.ascontiguousarray(inp[k]) for k in ("psi", "psi_prev", "u", "x")}
-        torch.cuda.synchronize()
-        t_e2e = []
-        for s in range(args.e2e_steps + 1):
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                bu_h, bpsi_h, cl = residual(disc, cfg.alphas[s % len(cfg.alphas)], hp["psi_prev"],
-                                            hp["u"], hp["psi"])
-                Dm = disc.assemble_D(hp["psi"]) if cached else None
-                for _ in range(kmv):
-                    y_h = (Dm @ hp["x"]) if cached else disc.apply_D(hp["psi"], hp["x"])
-            torch.cuda.synchronize()
-            if s > 0:
-                t_e2e.append(time.perf_counter() - t0)
-        h2d = 8 * reps * (2 * disc.ndof_psi + disc.ndof_u + (disc.ndof_psi if cached else 0)
-                          + kmv * disc.ndof_psi * (1 if cached else 2))
-        d2h = 8 * reps * (disc.ndof_u + disc.ndof_psi + kmv * disc.ndof_psi) + 4 * reps
-        e2e = {"value": eqp_step / statistics.mean(t_e2e) * world, "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": 1e3 * statistics.mean(t_e2e),
-               "ms_per_step_min_median_max": [1e3 * min(t_e2e), 1e3 * statistics.median(t_e2e), 1e3 * max(t_e2e)],
-               "path": "paper_2412_13733_b200.proximal.residual + disc.assemble_D + (D @ x) x k_mv, NumPy in/out"}
-
-    # element-block assembly (reported separately): configs whose
-    # BASELINE workload includes it
-    blocks = None
-    if cfg.name in ("c0", "c2", "c3") and world == 1:
-        disc.residual_t(cfg.alphas[0], psi_prev, u, psi, b_u=b_u, b_psi=b_psi, flag=flag, wcache=True)
-        nbl = disc.plan.block_len
-        chunk = max(1, min(cfg.N, int((8 << 30) // (8 * nbl))))      # <= 8 GB of blocks per launch
-        out_blk = torch.empty((chunk, nbl), dtype=torch.float64, device=dev)
-        disc.blocks_t(out=out_blk, c0=0, count=chunk)
-        torch.cuda.synchronize()
-        eb0 = torch.cuda.Event(enable_timing=True)
-        eb1 = torch.cuda.Event(enable_timing=True)
-        eb0.record()
-        for c0 in range(0, cfg.N, chunk):
-            disc.blocks_t(out=out_blk, c0=c0, count=min(chunk, cfg.N - c0))
-        eb1.record()
-        torch.cuda.synchronize()
-        t_blk = eb0.elapsed_time(eb1) * 1e-3
-        nb_ = cfg.ncomp * disc.n * disc.n
-        nbfield = 1 if cfg.kind == "obstacle" else 3
-        F_blk = cfg.N * nbfield * (2.0 * disc.n ** 4 * nq + 2.0 * disc.n ** 2 * nq ** 2)
-        B_blk = 8.0 * cfg.N * nb_ * nb_ + 8.0 * disc.ndof_psi
-        t_lb = max(F_blk / (P_FP64_TFLOPS * 1e12), B_blk / (hbm * 1e9))
-        blocks = {"ms": t_blk * 1e3, "tflops": F_blk / t_blk / 1e12, "gbs": B_blk / t_blk / 1e9,
-                  "roofline_frac": t_lb / t_blk, "bytes": B_blk, "flops": F_blk}
-        del out_blk
-
-    # per-cell Schur preconditioner (not part of the
-    # headline workload): P blocks from the cached weights, batched LU, solve
-    from paper_2412_13733_b200 import _lib
-    precond = None
-    if world == 1 and cfg.ncomp * disc.n * disc.n <= _lib.load().hpgLUMaxBlock():
-        precond = precond_timing(disc, cfg, psi_prev, u, psi, x, b_u, b_psi, flag, hbm)
-
-    # Schur-reduced Newton linear solve on the device
-    # (needs the per-cell preconditioner: config 3's 6561^2 blocks exceed the
-    # per-CTA LU, hpgLUMaxBlock, and are reported as unsupported, not timed)
-    lu_fits = cfg.ncomp * disc.n * disc.n <= _lib.load().hpgLUMaxBlock()
-    schur_info = None
-    if world == 1 and disc.plan.ndof_u > 0:
-        schur_info = (schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag) if lu_fits else
-                      {"unsupported": "per-cell LU block side exceeds hpgLUMaxBlock()"})
-
-    # the whole penalty continuation (proximal.solve) on the device, obstacle configs
-    solve_info = None
-    if world == 1 and cfg.kind == "obstacle":
-        solve_info = (solve_timing(disc) if lu_fits else
-                      {"unsupported": "per-cell LU block side exceeds hpgLUMaxBlock()"})
+                rec = gpu_config(CONFIGS[name], rule, args, local, world, full=False, e2e_steps=2)
+            per[name] = {k: rec[k] for k in ("value", "ms_per_step", "step_roofline_frac", "gpu_launches",
+                                                "buffer_sets")}
+            per[name]["roofline"] = {k: rec["roofline"][k] for k in ("kernel", "bound", "achieved", "peak",
+                                                                     "unit", "frac", "avg_launch_us")}
+            per[name]["e2e"] = rec["e2e"]["value"] if rec["e2e"] else None
+            per[name]["workload"] = rec["config"]["workload"]
+            if "blocks" in rec:
+                per[name]["blocks"] = rec["blocks"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            dt, eqp, desc = cpu_reference_step(cfg, rule)
-            cpu = {"value": eqp / dt, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                   "sample": desc, "seconds": dt}
+            cpu = reference_baseline(cfg, rule, one_thread=True)
         except Exception as exc:      # the baseline must never sink the GPU line
-            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
-                   "sample": f"failed: {exc!r}"}
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc!r}"}
+        for name in per:
+            if name == cfg.name:
+                per[name]["cpu_baseline"] = cpu.get("value")
+                continue
+            try:
+                c = reference_baseline(CONFIGS[name], rule, reps=1, one_thread=False)
+                per[name]["cpu_baseline"] = c["value"]
+                per[name]["cpu_baseline_as_is"] = c["as_is_value"]
+            except Exception as exc:
+                per[name]["cpu_baseline"] = f"failed: {exc!r}"
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inputs with the config's shapes and value laws, SURVEY.md §8d)",
-            "config": config_dict(cfg, rule),
-            "roofline": roof,
-            "step_roofline_frac": step_frac,
-            "blocks": blocks,
-            "precond": precond,
-            "schur": schur_info,
-            "solve": solve_info,
+            "config": head["config"],
+            "parallelism": "replicas" if world > 1 else "single GPU",
+            "roofline": head["roofline"],
+            "step_roofline_frac": head["step_roofline_frac"],
+            "precond": head.get("precond"),
+            "schur": head.get("schur"),
             "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
-            "res_ms_mean": statistics.mean(res_ms),
-            "mv_ms_mean": statistics.mean(mv_ms) if mv_ms else None,
+            "e2e": head["e2e"],
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
+            "res_ms_mean": head["res_ms_mean"],
+            "mv_ms_mean": head["mv_ms_mean"],
+            "per_config": per or None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

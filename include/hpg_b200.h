@@ -26,6 +26,17 @@
  *  - Clamp flags (`clamped`) are device ints; the call ORs 1 into *clamped
  *    when exp(-v) overflows the reference's clamp (assembly.py:187-192);
  *    the caller zeroes it.
+ *  - Concurrency: a plan owns device scratch (U-side edge contributions,
+ *    split partials, Schur / fast-diagonalisation work vectors, QVI tiles)
+ *    that its entry points overwrite.  A plan is therefore NOT re-entrant:
+ *    issue its calls on one stream at a time (or order the streams with
+ *    events); use one plan per concurrent stream.  Distinct plans are
+ *    independent.  The host-side launch caches are per device and locked,
+ *    so plans may be created and used from several host threads and devices.
+ *  - Allocation: hpgPlanCreate sizes every workspace of the hot entry points
+ *    (moments, applies, residuals, blocks, preconditioner factor / solve);
+ *    the one-time setups hpgPrecondPrepare, hpgStiffnessFactor and
+ *    hpgUFullSetup allocate their own tables.
  */
 #ifndef HPG_B200_H
 #define HPG_B200_H
@@ -167,7 +178,8 @@ int hpgLUProfile(unsigned long long* counters);
  * A = Kx(x)My + Mx(x)Ky, assembly.py:42-78, 470-474).  HOST inputs: the 1D
  * generalized eigenpairs Kx Vx = Mx Vx diag(lx), Vx^T Mx Vx = I (nix x nix
  * row-major, nix) and the same in y (schur.py: u_matrices_1d + eigh).
- * hpgStiffnessSolve: x = A^{-1} b on interior U vectors (four cuBLAS DGEMMs).
+ * hpgStiffnessSolve: x = A^{-1} b on interior U vectors (four DGEMMs on the
+ * FP64 tensor cores, the library's own k_dgemm_nn).
  * hpgSchurApply: SchurOperator.matvec (linalg.py:223-229) in one call,
  *   y = -((D x + E_beta x) + B^T A^{-1} B x / alpha), D from cached weights. */
 int hpgStiffnessFactor(hpgPlan plan, const double* Vx, const double* lx,
@@ -196,6 +208,39 @@ int hpgUFullOperator(hpgPlan plan, double gamma, const double* v,
                      const double* w, const double* rhs, double* out,
                      void* stream);
 int hpgUFullSolve(hpgPlan plan, const double* b, double* x, void* stream);
+
+/* Device GMRES (replaces linalg.gmres,
+ * linalg.py:134-207): unrestarted, Givens-rotated, the reference's stopping
+ * rule (relative to the initial residual in the minimised norm) and happy-
+ * breakdown test; CGS2 orthogonalisation.  The whole iteration is one CUDA
+ * graph with a device-side WHILE node: no host synchronisation per iteration
+ * and no operator application after convergence.
+ *
+ *   hpgGmresCreate(&g, n, maxiter)   Krylov basis + state (device)
+ *   hpgGmresBind(g, r, vin, w)       caller-owned device vectors of length n:
+ *       r = initial residual (already preconditioned for left
+ *       preconditioning; read by every solve), vin = input of the operator
+ *       chain, w = its output.  Rebinding drops the captured loop.
+ *   hpgGmresCaptureBegin(g, stream) ... the caller enqueues its operator
+ *       chain vin -> w on `stream` (right: w = A M vin, left: w = M A vin);
+ *       every call must be capturable (no synchronisation, no allocation) ...
+ *   hpgGmresCaptureEnd(g, stream)    appends the Arnoldi / Givens kernels
+ *   hpgGmresSolve(g, rtol, atol, dx, stream)
+ *       runs the loop on r and writes dx = V_k y_k (the caller applies M to
+ *       dx for right preconditioning and adds x0)
+ *   hpgGmresStatus(g, &iters, &converged, residuals[iters+1], stream)
+ *       synchronises `stream` and reports the last solve.
+ * `stream` must not be the legacy default stream (it is captured). */
+typedef struct hpgGmres_st* hpgGmres;
+int hpgGmresCreate(hpgGmres* g, long long n, int maxiter);
+int hpgGmresDestroy(hpgGmres g);
+int hpgGmresBind(hpgGmres g, const double* r, double* vin, double* w);
+int hpgGmresCaptureBegin(hpgGmres g, void* stream);
+int hpgGmresCaptureEnd(hpgGmres g, void* stream);
+int hpgGmresSolve(hpgGmres g, double rtol, double atol, double* dx, void* stream);
+int hpgGmresStatus(hpgGmres g, int* iters, int* converged, double* residuals, void* stream);
+/* out = a x + b y on device vectors (x or y may be NULL when its factor is 0). */
+int hpgAxpby(long long n, double a, const double* x, double b, const double* y, double* out, void* stream);
 
 const char* hpgLastError(void);
 int hpgVersion(void);

@@ -135,15 +135,15 @@ def case(name, kind, xpts, ypts, p, rule, Q=None, alpha=1.0, phi=phi_sin,
 
 
 def solve_case(name, kind, nc, p, rule, Q=None, phi=phi_sin, beta=1e-3, alpha_max=8.0,
-               line_search=False):
+               line_search=False, linear_solver="schur"):
     """The reference's whole penalty continuation (proximal.solve) from zero."""
     pts = np.linspace(0.0, 1.0, nc + 1)
     disc, t = build(kind, pts, pts, p, rule, Q, 1.0, phi)
     sched = proximal.AlphaSchedule(alpha0=1.0, rate=2.0, alpha_max=alpha_max)
-    opts = proximal.SolverOptions(line_search=line_search)
+    opts = proximal.SolverOptions(line_search=line_search, linear_solver=linear_solver)
     rep = proximal.solve(disc, sched, beta, opts)
     out = dict(kind=kind, xpts=pts, ypts=pts, p=p, rule=rule, nq=t.nq, alpha=1.0, beta=beta,
-               alpha_max=alpha_max, line_search=line_search,
+               alpha_max=alpha_max, line_search=line_search, linear_solver=linear_solver,
                S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi,
                u=rep.u, psi=rep.psi, multiplier=rep.multiplier,
                outer_increment=rep.outer_increment, converged=rep.converged,
@@ -182,7 +182,55 @@ def qvi_case(name, nc, p, rule, Q=None, load=100.0, scale=0.05):
     print(f"qvi/{name}: nfull={nf} newton={newton} gmres={gmres_its}")
 
 
+def solve_cases_r02():
+    """Round-2 continuations: the monolithic solver and the gradient constraint,
+    for the drop-in tests (tests/test_gpu_dropin.py)."""
+    solve_case("obst_p4_mono_ref", "obstacle", 4, 4, "reference", linear_solver="monolithic")
+    solve_case("obst_p5_mono_gauss", "obstacle", 3, 5, "gauss", Q=8, linear_solver="monolithic")
+    grad_solve_case("grad_p2_ref", 4, 2, "reference")
+    grad_solve_case("grad_p3_mono_gauss", 4, 3, "gauss", Q=6, linear_solver="monolithic")
+
+
+def grad_solve_case(name, nc, p, rule, Q=None, linear_solver="schur"):
+    """The reference CLI's gradient2d study settings (cli.py:321-360): the
+    GradientFrame2D data with cellwise phi, alpha 2^-7 * sqrt(2)^k up to 4,
+    Newton rtol 3e-5, GMRES rtol 1e-3, beta = 10^(-p + log2 h)."""
+    import math
+
+    from hpgalerkin.problems import GradientFrame2D
+    prob = GradientFrame2D()
+    pts = np.linspace(0.0, 1.0, nc + 1)
+    mesh = TensorMesh2D(Mesh1D(pts, np.full(nc, p)), Mesh1D(pts, np.full(nc, p)))
+    disc = GradientDisc2D(mesh, prob.f, prob.phi, phi_mode="cellwise")
+    if rule == "gauss":
+        t = substitute_gauss(disc, Q)
+        disc.f_load = disc.load_vector(prob.f)
+        disc.phi_values = {c: _eval_data(prob.phi, disc.kernels[c], "cellwise", 2)
+                           for c in disc.cell_ids}
+    else:
+        t = tb.Tables("reference", p, p)
+    sched = proximal.AlphaSchedule(alpha0=2.0 ** -7, rate=math.sqrt(2.0), alpha_max=4.0)
+    opts = proximal.SolverOptions(newton_rtol=3e-5, newton_atol=1e-13, gmres_rtol=1e-3,
+                                  linear_solver=linear_solver)
+    beta = 10.0 ** (-p + math.log2(1.0 / nc))
+    rep = proximal.solve(disc, sched, beta, opts)
+    out = dict(kind="gradient", xpts=pts, ypts=pts, p=p, rule=rule, nq=t.nq, alpha=2.0 ** -7,
+               beta=beta, alpha_max=4.0, line_search=False, linear_solver=linear_solver,
+               S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi,
+               u=rep.u, psi=rep.psi, multiplier=rep.multiplier,
+               outer_increment=rep.outer_increment, converged=rep.converged,
+               newton_iters=np.array([s.newton_iters for s in rep.steps]),
+               gmres_iters=np.array([sum(s.gmres_iters) for s in rep.steps]),
+               alphas=np.array([s.alpha for s in rep.steps]))
+    path = os.path.join(OUT, "solve", f"{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"solve/{name}: newton {out['newton_iters'].tolist()} gmres {out['gmres_iters'].tolist()}")
+
+
 def main():
+    if "--r02" in sys.argv:
+        solve_cases_r02()
+        return
     os.makedirs(OUT, exist_ok=True)
     u4 = np.linspace(0.0, 1.0, 5)
     u2 = np.linspace(0.0, 1.0, 3)

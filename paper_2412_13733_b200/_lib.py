@@ -52,6 +52,14 @@ SIGNATURES = {
     "hpgUFullValues": [_P, _P, _P, _P],
     "hpgUFullOperator": [_P, _D, _P, _P, _P, _P, _P],
     "hpgUFullSolve": [_P, _P, _P, _P],
+    "hpgGmresCreate": [ctypes.POINTER(_P), ctypes.c_longlong, _I],
+    "hpgGmresDestroy": [_P],
+    "hpgGmresBind": [_P, _P, _P, _P],
+    "hpgGmresCaptureBegin": [_P, _P],
+    "hpgGmresCaptureEnd": [_P, _P],
+    "hpgGmresSolve": [_P, _D, _D, _P, _P],
+    "hpgGmresStatus": [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), _P, _P],
+    "hpgAxpby": [ctypes.c_longlong, _D, _P, _D, _P, _P, _P],
     "hpgVersion": [],
 }
 

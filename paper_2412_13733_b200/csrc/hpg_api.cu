@@ -1,7 +1,10 @@
 // C ABI of the B200 hpG element-quadrature engine (see include/hpg_b200.h).
 // Host side of the library: plan construction (fragment-ordered tables on the
 // device), path selection and kernel launches.  No allocation in the hot
-// entry points: every workspace is sized at plan creation.
+// entry points: every workspace is sized at plan creation (the optional
+// solver setups -- hpgPrecondPrepare, hpgStiffnessFactor, hpgUFullSetup --
+// allocate their own once).  A plan owns its scratch, so one plan must not be
+// used from two streams at the same time (see include/hpg_b200.h).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -17,7 +20,7 @@
 #include "hpg_schur.cuh"
 #include "hpg_qvi.cuh"
 
-#include <cublas_v2.h>
+#include "hpg_gemm.cuh"
 #include "hpg_useside.cuh"
 #include "hpg_small.cuh"
 #include "hpg_ucell.cuh"
@@ -104,21 +107,22 @@ struct hpgPlan_st {
 
   // fast-diagonalisation solves: interior stiffness A (fdm[0]) and the QVI
   // full-space H = A_full + gamma M_full (fdm[1]); Schur apply scratch
-  cublasHandle_t cub = nullptr;
   struct Fdm {
     int r = 0, c = 0;
-    double *Vx = nullptr, *Vy = nullptr, *finv = nullptr, *w1 = nullptr, *w2 = nullptr;
+    double *Vx = nullptr, *Vy = nullptr, *VxT = nullptr, *VyT = nullptr, *finv = nullptr, *w1 = nullptr,
+           *w2 = nullptr;
     bool ready = false;
     void release() {
-      cudaFree(Vx); cudaFree(Vy); cudaFree(finv); cudaFree(w1); cudaFree(w2);
-      Vx = Vy = finv = w1 = w2 = nullptr;
+      cudaFree(Vx); cudaFree(Vy); cudaFree(VxT); cudaFree(VyT); cudaFree(finv); cudaFree(w1); cudaFree(w2);
+      Vx = Vy = VxT = VyT = finv = w1 = w2 = nullptr;
       ready = false;
     }
   } fdm[2];
   double *su1 = nullptr, *su2 = nullptr, *syD = nullptr, *sz = nullptr;
   bool fdm_ready = false;
   // QVI full-space operator tables and scratch
-  double *qSR = nullptr, *qTR = nullptr, *qK = nullptr, *qM = nullptr;
+  double *qSR = nullptr, *qTR = nullptr, *qK = nullptr, *qM = nullptr, *qSRT = nullptr, *qTRT = nullptr;
+  double *qKT = nullptr, *qMT = nullptr;
   double *qC = nullptr, *qT = nullptr, *qV = nullptr, *qG = nullptr, *qP1 = nullptr, *qP2 = nullptr;
   double *qH1 = nullptr, *qH2 = nullptr, *qH3 = nullptr;
   bool q_ready = false;
@@ -160,6 +164,29 @@ template <int MODE>
 int run_elem(hpgPlan_st* P, ElemArgs A, cudaStream_t s) {
   if (!P->use_warp[MODE]) A.splits = P->splits;
   return run_mode<MODE>(P->use_warp[MODE] != 0, A, s);
+}
+
+// shared memory of the block-row kernel (k_blockrow, 4 warps): PK(G) staged
+// when it fits, else read from L2 (*pk_smem = 0)
+size_t blockrow_smem(const hpgPlan_st* P, int* pk_smem) {
+  const int threads = 128;
+  const size_t zs = sizeof(double) * (size_t)P->NT * P->QT * 64;
+  const size_t pks = sizeof(double) * (size_t)P->n * P->NT * 2 * P->QT * 32;
+  const size_t so = sizeof(double) * (size_t)(8 * P->NT) * (8 * P->NT + 1);
+  size_t smem = pks + (zs + so) * (threads / 32);
+  *pk_smem = 1;
+  if (smem > ((size_t)200 << 10) && P->NT <= 4) {
+    *pk_smem = 0;
+    smem = (zs + so) * (threads / 32);
+  }
+  return smem;
+}
+
+// large tiles: element blocks as two GEMMs (Z = G W, blocks = Z G^T) through
+// the plan's global scratch instead of the block-row kernel
+bool blocks_use_gemm(const hpgPlan_st* P) {
+  int pk;
+  return blockrow_smem(P, &pk) > ((size_t)200 << 10) || P->NT > 4;
 }
 
 int check(hpgPlan p) {
@@ -223,23 +250,23 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (P->n > 128 || nq > 256) { delete P; return fail(HPG_ERR_UNSUPPORTED, "n > 128 or nq > 256"); }
+  if (P->n > 128 || nq > 256) { hpgPlanDestroy(P); return fail(HPG_ERR_UNSUPPORTED, "n > 128 or nq > 256"); }
 
   std::vector<double> sf = pk_table(S, nq, P->n, P->QT, P->NP);
   std::vector<double> tf = pk_table(T, P->n, nq, P->NT, P->QP);
   int rc;
-  if ((rc = upload(&P->Sf, sf.data(), sf.size()))) { delete P; return rc; }
-  if ((rc = upload(&P->Tf, tf.data(), tf.size()))) { delete P; return rc; }
-  if ((rc = upload(&P->hx, hx, ncx))) { delete P; return rc; }
-  if ((rc = upload(&P->hy, hy, ncy))) { delete P; return rc; }
+  if ((rc = upload(&P->Sf, sf.data(), sf.size()))) { hpgPlanDestroy(P); return rc; }
+  if ((rc = upload(&P->Tf, tf.data(), tf.size()))) { hpgPlanDestroy(P); return rc; }
+  if ((rc = upload(&P->hx, hx, ncx))) { hpgPlanDestroy(P); return rc; }
+  if ((rc = upload(&P->hy, hy, ncy))) { hpgPlanDestroy(P); return rc; }
   P->hxh.assign(hx, hx + ncx);
   P->hyh.assign(hy, hy + ncy);
   // u side (load_vector): analysis with Tu, tile side m
   P->NTu = (P->m + 7) / 8;
   std::vector<double> tuf = pk_table(Tu, P->m, nq, P->NTu, P->QP);
   std::vector<double> suf = pk_table(Su, nq, P->m, P->QT, 8 * P->NTu);
-  if ((rc = upload(&P->Tuf, tuf.data(), tuf.size()))) { delete P; return rc; }
-  if ((rc = upload(&P->Suf, suf.data(), suf.size()))) { delete P; return rc; }
+  if ((rc = upload(&P->Tuf, tuf.data(), tuf.size()))) { hpgPlanDestroy(P); return rc; }
+  if ((rc = upload(&P->Suf, suf.data(), suf.size()))) { hpgPlanDestroy(P); return rc; }
   // low-degree obstacle path (config 4): tables passed by value to k_small
   memset(&P->stab, 0, sizeof(P->stab));
   if (kind == HPG_OBSTACLE && P->n <= SMALL_MAXN && nq <= SMALL_MAXQ && small_available(P->n, nq)) {
@@ -256,7 +283,7 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
     for (int j = 0; j < P->n; ++j)
       for (int g = 0; g < nq; ++g)
         G[((size_t)a * P->n + j) * P->QP + g] = T[(size_t)a * nq + g] * S[(size_t)g * P->n + j];
-  if ((rc = upload(&P->G, G.data(), G.size()))) { delete P; return rc; }
+  if ((rc = upload(&P->G, G.data(), G.size()))) { hpgPlanDestroy(P); return rc; }
   {
     // PK(G)[b][nt][ks][lane] = G[(b, k = 8nt + r)][h = 8(ks>>1) + 2c + (ks&1)]
     const int QK = 2 * P->QT;
@@ -270,13 +297,13 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
             if (k < P->n && h < nq)
               pkg[(((size_t)b * P->NT + nt) * QK + ks) * 32 + lane] = G[((size_t)b * P->n + k) * P->QP + h];
           }
-    if ((rc = upload(&P->PKG, pkg.data(), pkg.size()))) { delete P; return rc; }
+    if ((rc = upload(&P->PKG, pkg.data(), pkg.size()))) { hpgPlanDestroy(P); return rc; }
   }
   cudaError_t e = cudaMalloc(&P->scratch_u, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
   if (e == cudaSuccess) e = cudaMalloc(&P->mu, sizeof(double) * (size_t)P->N * P->m * P->m + 16);
   if (e == cudaSuccess) e = cudaMalloc(&P->dflag, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&P->edge, sizeof(double) * (size_t)P->N * (4 * P->m - 4) + 16);
-  if (e != cudaSuccess) { delete P; return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+  if (e != cudaSuccess) { hpgPlanDestroy(P); return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
 
   // path selection
   P->use_warp[M_OBST_RES] = warp_fits(M_OBST_RES, P->NT, P->QT);
@@ -300,7 +327,18 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   size_t plu = (size_t)P->N * P->splits * NPu * NPu;
   if (plu > P->partial_len) P->partial_len = plu;
   e = cudaMalloc(&P->partial, sizeof(double) * P->partial_len + 16);
-  if (e != cudaSuccess) { delete P; return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+  if (e != cudaSuccess) { hpgPlanDestroy(P); return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+  // element blocks of large tiles run as two GEMMs through a stage-1 scratch
+  // (<= 256 MB, whole cells): sized here so hpgBlocks never allocates
+  if (blocks_use_gemm(P)) {
+    const size_t per_cell = (size_t)(kind == HPG_OBSTACLE ? 1 : 3) * n2 * P->QP;
+    long long chunk = (long long)((256ull << 20) / (sizeof(double) * per_cell));
+    if (chunk < 1) chunk = 1;
+    if (chunk > P->N) chunk = P->N;
+    e = cudaMalloc(&P->Z, sizeof(double) * per_cell * chunk + 16);
+    if (e != cudaSuccess) { hpgPlanDestroy(P); return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+    P->zcells = (int)chunk;
+  }
   *plan = P;
   return HPG_OK;
 }
@@ -315,8 +353,7 @@ int hpgPlanDestroy(hpgPlan P) {
   cudaFree(P->su1); cudaFree(P->su2); cudaFree(P->syD); cudaFree(P->sz);
   cudaFree(P->qSR); cudaFree(P->qTR); cudaFree(P->qK); cudaFree(P->qM); cudaFree(P->qC); cudaFree(P->qT);
   cudaFree(P->qV); cudaFree(P->qG); cudaFree(P->qP1); cudaFree(P->qP2); cudaFree(P->qH1); cudaFree(P->qH2);
-  cudaFree(P->qH3);
-  if (P->cub) cublasDestroy(P->cub);
+  cudaFree(P->qH3); cudaFree(P->qSRT); cudaFree(P->qTRT); cudaFree(P->qKT); cudaFree(P->qMT);
   delete P;
   return HPG_OK;
 }
@@ -504,16 +541,7 @@ static int blocks_gemm(hpgPlan P, const double* wcache, double* blocks, int c0, 
   int nf = P->kind == HPG_OBSTACLE ? 1 : 3;
   int n2 = P->n * P->n;
   // stage-1 scratch sized for up to 256 MB of Z per pass
-  size_t per_cell = (size_t)nf * n2 * P->QP;
-  int chunk = (int)((256ull << 20) / (sizeof(double) * per_cell));
-  if (chunk < 1) chunk = 1;
-  if (chunk > P->N) chunk = P->N;
-  if (P->Z == nullptr || P->zcells < chunk) {
-    cudaFree(P->Z);
-    P->Z = nullptr;
-    CUDA_TRY(cudaMalloc(&P->Z, sizeof(double) * per_cell * chunk + 16));
-    P->zcells = chunk;
-  }
+  if (P->Z == nullptr || P->zcells < 1) return fail(HPG_ERR_UNSUPPORTED, "block GEMM scratch was not sized for this plan");
   GemmArgs g;
   memset(&g, 0, sizeof(g));
   g.nfield = nf; g.n = P->n; g.n2 = n2; g.QP = P->QP; g.QT = P->QT; g.NW = nf;
@@ -556,17 +584,10 @@ static int blocks_impl(hpgPlan P, const double* wcache, double* blocks, int c0, 
   B.hx = P->hx; B.hy = P->hy;
   B.per_warp = 1;
   const int threads = 128;
-  const size_t zs = sizeof(double) * (size_t)P->NT * P->QT * 64;
-  const size_t pks = sizeof(double) * (size_t)P->n * P->NT * 2 * P->QT * 32;
-  const size_t so = sizeof(double) * (size_t)(8 * P->NT) * (8 * P->NT + 1);
-  size_t smem = pks + (zs + so) * (threads / 32);
-  B.pk_smem = 1;
-  if (smem > ((size_t)200 << 10) && P->NT <= 4) {
-    // PK(G) too large to stage: read it from L2 (shared by every cell)
-    B.pk_smem = 0;
-    smem = (zs + so) * (threads / 32);
-  }
-  if (smem > ((size_t)200 << 10) || P->NT > 4) {
+  int pk_smem = 1;
+  size_t smem = blockrow_smem(P, &pk_smem);
+  B.pk_smem = pk_smem;
+  if (blocks_use_gemm(P)) {
     // large tiles: two-stage GEMM (Z = G W, blocks = Z G^T) through global scratch
     int rc = blocks_gemm(P, wcache, blocks, c0, count, s);
     if (rc || !prec) return rc;
@@ -801,25 +822,27 @@ int hpgLUProfile(unsigned long long* counters) {
 // ---------------------------------------------------------------------------
 // Fast-diagonalisation stiffness solve and the Schur operator (linalg.py:100-117, 213-229)
 
-#define CUBLAS_TRY(x)                                                                   \
-  do {                                                                                  \
-    cublasStatus_t _st = (x);                                                           \
-    if (_st != CUBLAS_STATUS_SUCCESS)                                                   \
-      return fail(HPG_ERR_CUDA, std::string(#x) + ": cublas status " + std::to_string((int)_st)); \
-  } while (0)
+static std::vector<double> transposed(const double* X, int rows, int cols) {
+  std::vector<double> t((size_t)rows * cols);
+  for (int i = 0; i < rows; ++i)
+    for (int j = 0; j < cols; ++j) t[(size_t)j * rows + i] = X[(size_t)i * cols + j];
+  return t;
+}
 
 static int fdm_setup(hpgPlan P, int slot, int r, int c, const double* Vx, const double* lx, const double* Vy,
                      const double* ly, double shift) {
-  if (P->cub == nullptr) CUBLAS_TRY(cublasCreate(&P->cub));
   auto& F = P->fdm[slot];
   F.release();
   F.r = r; F.c = c;
   std::vector<double> finv((size_t)r * c);
   for (long long i = 0; i < r; ++i)
     for (long long j = 0; j < c; ++j) finv[(size_t)(i * c + j)] = 1.0 / (lx[i] + ly[j] + shift);
+  std::vector<double> vxt = transposed(Vx, r, r), vyt = transposed(Vy, c, c);
   int rc;
   if ((rc = upload(&F.Vx, Vx, (size_t)r * r))) return rc;
   if ((rc = upload(&F.Vy, Vy, (size_t)c * c))) return rc;
+  if ((rc = upload(&F.VxT, vxt.data(), vxt.size()))) return rc;
+  if ((rc = upload(&F.VyT, vyt.data(), vyt.size()))) return rc;
   if ((rc = upload(&F.finv, finv.data(), finv.size()))) return rc;
   CUDA_TRY(cudaMalloc(&F.w1, sizeof(double) * (size_t)r * c + 16));
   CUDA_TRY(cudaMalloc(&F.w2, sizeof(double) * (size_t)r * c + 16));
@@ -845,37 +868,28 @@ int hpgStiffnessFactor(hpgPlan P, const double* Vx, const double* lx, const doub
   return HPG_OK;
 }
 
-// row-major C (M x N) = op(A) op(B) through column-major cuBLAS
-static int rm_gemm(hpgPlan P, bool ta, bool tb, int M, int N, int K, const double* A, int lda, const double* B,
-                   int ldb, double* C, int ldc) {
-  const double one = 1.0, zero = 0.0;
-  CUBLAS_TRY(cublasDgemm(P->cub, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K, &one,
-                         B, ldb, A, lda, &zero, C, ldc));
+// row-major C (M x N) = A (M x K) B (K x N) (.* F), batched with strides
+// (stride 0 = operand shared by the batch): k_dgemm_nn, hpg_gemm.cuh
+static int gemm(int M, int N, int K, const double* A, long long lda, long long sA, const double* B, long long ldb,
+                long long sB, double* C, long long ldc, long long sC, int batch, cudaStream_t s,
+                const double* F = nullptr) {
+  GemmNN g = gemm_nn(M, N, K, A, lda, B, ldb, C, ldc);
+  g.sA = sA; g.sB = sB; g.sC = sC;
+  g.F = F; g.sF = 0;
+  CUDA_TRY(dgemm_nn(g, batch, s));
   return HPG_OK;
 }
 
-// the same, batched with strides (stride 0 = shared operand)
-static int rm_gemm_batched(hpgPlan P, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
-                           long long sA, const double* B, int ldb, long long sB, double* C, int ldc, long long sC,
-                           int batch) {
-  const double one = 1.0, zero = 0.0;
-  CUBLAS_TRY(cublasDgemmStridedBatched(P->cub, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N,
-                                       M, K, &one, B, ldb, sB, A, lda, sA, &zero, C, ldc, sC, batch));
-  return HPG_OK;
-}
-
+// A^{-1} b = Vx [(Vx^T B Vy) ./ (lx + ly)] Vy^T: four GEMMs, the scaling fused
+// into the second one's epilogue
 static int fdm_solve(hpgPlan P, int slot, const double* b, double* x, cudaStream_t s) {
   auto& F = P->fdm[slot];
   const int r = F.r, c = F.c;
-  CUBLAS_TRY(cublasSetStream(P->cub, s));
   int rc;
-  if ((rc = rm_gemm(P, true, false, r, c, r, F.Vx, r, b, c, F.w1, c))) return rc;        // Vx^T B
-  if ((rc = rm_gemm(P, false, false, r, c, c, F.w1, c, F.Vy, c, F.w2, c))) return rc;    // . Vy
-  const long long n = (long long)r * c;
-  k_fdm_scale<<<(int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16), 256, 0, s>>>(F.w2, F.finv, n);
-  LAUNCH_CHECK();
-  if ((rc = rm_gemm(P, false, false, r, c, r, F.Vx, r, F.w2, c, F.w1, c))) return rc;    // Vx .
-  return rm_gemm(P, false, true, r, c, c, F.w1, c, F.Vy, c, x, c);                        // . Vy^T
+  if ((rc = gemm(r, c, r, F.VxT, r, 0, b, c, 0, F.w1, c, 0, 1, s))) return rc;             // Vx^T B
+  if ((rc = gemm(r, c, c, F.w1, c, 0, F.Vy, c, 0, F.w2, c, 0, 1, s, F.finv))) return rc;   // (. Vy) ./ (lx+ly)
+  if ((rc = gemm(r, c, r, F.Vx, r, 0, F.w2, c, 0, F.w1, c, 0, 1, s))) return rc;           // Vx .
+  return gemm(r, c, c, F.w1, c, 0, F.VyT, c, 0, x, c, 0, 1, s);                           // . Vy^T
 }
 
 static int stiffness_solve(hpgPlan P, const double* b, double* x, cudaStream_t s) {
@@ -925,13 +939,21 @@ int hpgUFullSetup(hpgPlan P, double gamma, const double* SR, const double* TR, c
   const int nfx = P->ncx * P->p + 1, nfy = P->ncy * P->p + 1;
   P->q_ready = false;
   double** bufs[] = {&P->qSR, &P->qTR, &P->qK, &P->qM, &P->qC, &P->qT, &P->qV, &P->qG,
-                     &P->qP1, &P->qP2, &P->qH1, &P->qH2, &P->qH3};
+                     &P->qP1, &P->qP2, &P->qH1, &P->qH2, &P->qH3, &P->qSRT, &P->qTRT, &P->qKT, &P->qMT};
   for (double** b : bufs) { cudaFree(*b); *b = nullptr; }
   int rc;
   if ((rc = upload(&P->qSR, SR, (size_t)Q * m))) return rc;
   if ((rc = upload(&P->qTR, TR, (size_t)m * Q))) return rc;
   if ((rc = upload(&P->qK, Kh, (size_t)m * m))) return rc;
   if ((rc = upload(&P->qM, Mh, (size_t)m * m))) return rc;
+  {
+    std::vector<double> srt = transposed(SR, Q, m), trt = transposed(TR, m, Q);
+    std::vector<double> kt = transposed(Kh, m, m), mt = transposed(Mh, m, m);
+    if ((rc = upload(&P->qSRT, srt.data(), srt.size()))) return rc;
+    if ((rc = upload(&P->qTRT, trt.data(), trt.size()))) return rc;
+    if ((rc = upload(&P->qKT, kt.data(), kt.size()))) return rc;
+    if ((rc = upload(&P->qMT, mt.data(), mt.size()))) return rc;
+  }
   const size_t mm = (size_t)N * m * m, qm = (size_t)N * Q * (Q > m ? Q : m), qq = (size_t)N * Q * Q;
   CUDA_TRY(cudaMalloc(&P->qC, sizeof(double) * mm + 16));
   CUDA_TRY(cudaMalloc(&P->qT, sizeof(double) * qm + 16));
@@ -963,13 +985,10 @@ static int q_values(hpgPlan P, const double* v, cudaStream_t s) {
   QArgs A = qargs(P);
   k_qgather<<<grid_for((long long)N * m * m), 256, 0, s>>>(A, v, P->qC);
   LAUNCH_CHECK();
-  CUBLAS_TRY(cublasSetStream(P->cub, s));
   int rc;
-  if ((rc = rm_gemm_batched(P, false, false, Q, m, m, P->qSR, m, 0, P->qC, m, (long long)m * m, P->qT, m,
-                            (long long)Q * m, N)))
-    return rc;
-  return rm_gemm_batched(P, false, true, Q, Q, m, P->qT, m, (long long)Q * m, P->qSR, m, 0, P->qV, Q,
-                         (long long)Q * Q, N);
+  // T = SR C (Q x m per cell), V = T SR^T (Q x Q per cell)
+  if ((rc = gemm(Q, m, m, P->qSR, m, 0, P->qC, m, (long long)m * m, P->qT, m, (long long)Q * m, N, s))) return rc;
+  return gemm(Q, Q, m, P->qT, m, (long long)Q * m, P->qSRT, Q, 0, P->qV, Q, (long long)Q * Q, N, s);
 }
 
 int hpgUFullValues(hpgPlan P, const double* v, double* vals, void* stream) {
@@ -991,25 +1010,23 @@ int hpgUFullOperator(hpgPlan P, double gamma, const double* v, const double* w, 
   cudaStream_t s = (cudaStream_t)stream;
   const int m = P->m, Q = P->nq, N = P->N;
   const long long mm = (long long)m * m, qq = (long long)Q * Q;
-  CUBLAS_TRY(cublasSetStream(P->cub, s));
   int rc;
   if (v) {
     if ((rc = q_values(P, v, s))) return rc;                 // C = tiles(v), V = values(v)
     // H terms: Kh C Mh, Mh C Kh, Mh C Mh
-    if ((rc = rm_gemm_batched(P, false, false, m, m, m, P->qK, m, 0, P->qC, m, mm, P->qP1, m, mm, N))) return rc;
-    if ((rc = rm_gemm_batched(P, false, false, m, m, m, P->qM, m, 0, P->qC, m, mm, P->qP2, m, mm, N))) return rc;
-    if ((rc = rm_gemm_batched(P, false, true, m, m, m, P->qP1, m, mm, P->qM, m, 0, P->qH1, m, mm, N))) return rc;
-    if ((rc = rm_gemm_batched(P, false, true, m, m, m, P->qP2, m, mm, P->qK, m, 0, P->qH2, m, mm, N))) return rc;
-    if ((rc = rm_gemm_batched(P, false, true, m, m, m, P->qP2, m, mm, P->qM, m, 0, P->qH3, m, mm, N))) return rc;
+    if ((rc = gemm(m, m, m, P->qK, m, 0, P->qC, m, mm, P->qP1, m, mm, N, s))) return rc;
+    if ((rc = gemm(m, m, m, P->qM, m, 0, P->qC, m, mm, P->qP2, m, mm, N, s))) return rc;
+    if ((rc = gemm(m, m, m, P->qP1, m, mm, P->qMT, m, 0, P->qH1, m, mm, N, s))) return rc;
+    if ((rc = gemm(m, m, m, P->qP2, m, mm, P->qKT, m, 0, P->qH2, m, mm, N, s))) return rc;
+    if ((rc = gemm(m, m, m, P->qP2, m, mm, P->qMT, m, 0, P->qH3, m, mm, N, s))) return rc;
   }
   const bool load = w || rhs;
   if (load) {
     k_qpoint<<<grid_for((long long)N * qq), 256, 0, s>>>((long long)N * qq, P->qV, w, rhs);
     LAUNCH_CHECK();
-    if ((rc = rm_gemm_batched(P, false, false, m, Q, Q, P->qTR, Q, 0, P->qV, Q, qq, P->qT, Q, (long long)m * Q, N)))
-      return rc;
-    if ((rc = rm_gemm_batched(P, false, true, m, m, Q, P->qT, Q, (long long)m * Q, P->qTR, Q, 0, P->qG, m, mm, N)))
-      return rc;
+    // G = TR V TR^T per cell
+    if ((rc = gemm(m, Q, Q, P->qTR, Q, 0, P->qV, Q, qq, P->qT, Q, (long long)m * Q, N, s))) return rc;
+    if ((rc = gemm(m, m, Q, P->qT, Q, (long long)m * Q, P->qTRT, m, 0, P->qG, m, mm, N, s))) return rc;
   }
   QArgs A = qargs(P);
   const long long nfull = ((long long)P->ncx * P->p + 1) * A.nfy;

@@ -151,7 +151,8 @@ __device__ __forceinline__ void map_pair_w(const double (&V)[NSYN > 0 ? NSYN : 1
 // Latency structure (one wave: the grid never exceeds the resident slots):
 //  * launched with programmatic stream serialization (PDL): the table fill
 //    into shared memory runs while the previous kernel drains, then
-//    griddepcontrol.wait orders every read of psi / x / weights after it;
+//    griddepcontrol.wait orders every read of psi / x / weights after it
+//    (the only reads issued before the wait are the constant tables);
 //  * small tiles (NIN*2*NT^2 <= 8 doubles) skip the shared-memory staging:
 //    each lane loads exactly the B-fragment entries C[8(ks>>1)+2c+(ks&1)][8nt+r]
 //    it feeds to the first contraction (rows of 8 consecutive doubles);
@@ -244,10 +245,10 @@ k_warp(ElemArgs A) {
   }
   cp_async_commit();
   for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
-  // cached modes: the point weights of the first cell are copied BEFORE the
-  // grid-dependency wait.  This is safe because no PDL kernel that writes a
-  // weight cache triggers its dependents early (the residual modes below), so
-  // a weight cache is always complete when a kernel reading it is launched.
+  // only the (constant) tables are copied before the grid-dependency wait:
+  // PDL makes the previous grid's writes visible after griddepcontrol.wait
+  // and not before, so the weight cache -- which the immediately preceding
+  // kernel may have written -- is read after it
   int buf = 0;
   // ROLL: one row tile's weights into half h of the warp's slice
   auto load_rt = [&](int e, int rt, int h) {
@@ -271,11 +272,10 @@ k_warp(ElemArgs A) {
   };
   const int stride = gridDim.x * W;
   int e = blockIdx.x * W + warp;
-  if (e < A.N) load_weights(e, 0);
-  // one wave: let the next kernel in the stream start its prologue now --
-  // except kernels that write a weight cache (see load_weights)
-  if constexpr (!CF::WRITES_WC) pdl_trigger();
+  // one wave: let the next kernel in the stream start its (table) prologue now
+  pdl_trigger();
   pdl_wait();
+  if (e < A.N) load_weights(e, 0);
 
   using XFrag = double[REGX ? NIN : 1][REGX ? NK : 1][REGX ? NT : 1];
   XFrag X, Xn;

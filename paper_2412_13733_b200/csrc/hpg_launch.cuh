@@ -2,6 +2,8 @@
 // (hpg_mode_*.cu) so the template instantiations compile in parallel.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <mutex>
 #include "hpg_common.cuh"
 #include "../../include/hpg_b200.h"
 
@@ -9,6 +11,24 @@ namespace hpg {
 
 int set_error(int code, const char* where, cudaError_t e);
 int set_error_msg(int code, const char* msg);
+
+// Launch-setup memo per device (function attributes and occupancy are per
+// device) behind a mutex, so plans on several devices / host threads share
+// the library safely.  T needs a default constructor marking "not set up".
+constexpr int kMaxDevices = 64;
+template <class T>
+struct PerDevice {
+  std::mutex mu;
+  T slot[kMaxDevices];
+  // run fn(T&) under the lock on the current device's slot
+  template <class F>
+  auto with(F&& fn) -> decltype(fn(slot[0])) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    return fn(slot[dev % kMaxDevices]);
+  }
+};
 
 // Is there a warp-per-element instantiation for (NT, QT) in this mode?
 template <int MODE> bool warp_available(int NT, int QT);

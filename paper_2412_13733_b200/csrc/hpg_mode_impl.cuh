@@ -20,24 +20,30 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   const size_t smem = sizeof(double) * (2 * QP * NP + W * (NSTAGE * NP * (NP + 2) + WDBL) + NP +
                                         (size_t)W * A.usmem);
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "warp path shared memory too large");
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_warp<NT, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_warp)", e);
-    attr = smem;
-  }
-  // persistent-style grid: every resident warp slot gets an equal share of cells
-  static int occ = -1, nsm = 0, occ_smem = -1;
-  if (occ < 0 || occ_smem != (int)smem) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp<NT, QT, MODE>, 32 * W, smem);
-    if (occ < 1) occ = 1;
-    occ_smem = (int)smem;
-  }
+  struct Memo { size_t attr = 0; int occ = -1, nsm = 0, occ_smem = -1; };
+  static PerDevice<Memo> memo;
+  int grid_cap = 0;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if (smem > m.attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_warp<NT, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      m.attr = smem;
+    }
+    // persistent-style grid: every resident warp slot gets an equal share of cells
+    if (m.occ < 0 || m.occ_smem != (int)smem) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&m.nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m.occ, k_warp<NT, QT, MODE>, 32 * W, smem);
+      if (m.occ < 1) m.occ = 1;
+      m.occ_smem = (int)smem;
+    }
+    grid_cap = m.nsm * m.occ;
+    return cudaSuccess;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_warp)", se);
   int need = (A.N + W * CF::CPW - 1) / (W * CF::CPW);
-  int grid = need < nsm * occ ? need : nsm * occ;
+  int grid = need < grid_cap ? need : grid_cap;
   // programmatic dependent launch: the table prologue overlaps the previous
   // kernel's tail (k_warp orders its data reads with griddepcontrol.wait)
   cudaLaunchConfig_t cfg = {};
@@ -76,22 +82,24 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
     }
   }
   if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "element tile too large for shared memory");
-  static int attr = 0;
-  if ((int)smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_cta)", e);
-    attr = (int)smem;
-  }
   // row-tile splits of a cell as one thread-block cluster (<= 8, portable):
   // partials reduced through DSMEM inside the kernel, when the clusters fit
-  // in one wave (checked once per shape)
+  // in one wave (checked once per shape and device)
+  struct Memo { int attr = 0; int ok_splits = -1, ok_n = -1, ok_np = -1, ok_res = 0; };
+  static PerDevice<Memo> memo;
   A.cluster_red = 0;
-  if (A.splits > 1 && A.splits <= 8 && getenv("HPG_NO_CLUSTER") == nullptr) {
-    const size_t ysmem = sizeof(double) * (size_t)TR::NOUT * NP * NP;
-    const size_t csmem = smem > ysmem ? smem : ysmem;
-    static int ok_splits = -1, ok_n = -1, ok_np = -1, ok_res = 0;
-    if (ok_splits != A.splits || ok_n != A.N || ok_np != NP) {
-      ok_splits = A.splits; ok_n = A.N; ok_np = NP; ok_res = 0;
+  const bool try_cluster = A.splits > 1 && A.splits <= 8 && getenv("HPG_NO_CLUSTER") == nullptr;
+  const size_t ysmem = sizeof(double) * (size_t)TR::NOUT * NP * NP;
+  const size_t csmem = smem > ysmem ? smem : ysmem;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if ((int)smem > m.attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      m.attr = (int)smem;
+    }
+    if (!try_cluster) return cudaSuccess;
+    if (m.ok_splits != A.splits || m.ok_n != A.N || m.ok_np != NP) {
+      m.ok_splits = A.splits; m.ok_n = A.N; m.ok_np = NP; m.ok_res = 0;
       if (csmem <= 227 * 1024 &&
           cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem) == cudaSuccess) {
         cudaLaunchConfig_t q = {};
@@ -105,30 +113,32 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
         q.numAttrs = 1;
         int nclusters = 0;
         cudaError_t qe = cudaOccupancyMaxActiveClusters(&nclusters, k_cta<MODE, MAXS, W>, &q);
-        if (qe == cudaSuccess && nclusters >= A.N) ok_res = 1;
+        if (qe == cudaSuccess && nclusters >= A.N) m.ok_res = 1;
         if (getenv("HPG_DEBUG"))
           fprintf(stderr, "[hpg] k_cta mode %d: %d cells x %d splits, smem %zu: max active clusters %d (%s) -> %s\n",
-                  MODE, A.N, A.splits, csmem, nclusters, cudaGetErrorString(qe), ok_res ? "cluster" : "reduce kernel");
+                  MODE, A.N, A.splits, csmem, nclusters, cudaGetErrorString(qe), m.ok_res ? "cluster" : "reduce kernel");
         cudaGetLastError();
-        if ((int)csmem > attr) attr = (int)csmem;
+        if ((int)csmem > m.attr) m.attr = (int)csmem;
       }
     }
-    if (ok_res) {
-      A.cluster_red = 1;
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3(A.N * A.splits);
-      q.blockDim = dim3(32 * W);
-      q.dynamicSmemBytes = smem > ysmem ? smem : ysmem;
-      q.stream = s;
-      cudaLaunchAttribute qa[1];
-      qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = A.splits; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
-      q.attrs = qa;
-      q.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&q, k_cta<MODE, MAXS, W>, A);
-      if (e == cudaSuccess) e = cudaGetLastError();
-      return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_cta cluster launch", e);
-    }
+    A.cluster_red = m.ok_res;
+    return cudaSuccess;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_cta)", se);
+  if (A.cluster_red) {
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(A.N * A.splits);
+    q.blockDim = dim3(32 * W);
+    q.dynamicSmemBytes = csmem;
+    q.stream = s;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = A.splits; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&q, k_cta<MODE, MAXS, W>, A);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_cta cluster launch", e);
   }
   cudaError_t e = launch_pdl(k_cta<MODE, MAXS, W>, dim3(A.N * A.splits), dim3(32 * W), smem, s, A);
   if (e == cudaSuccess) e = cudaGetLastError();

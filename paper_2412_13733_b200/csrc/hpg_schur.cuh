@@ -5,7 +5,8 @@
 //   linalg.factor_stiffness / SpluFactor.solve (linalg.py:100-117): with the
 //   1D generalized eigenpairs K V = M V diag(l), V^T M V = I,
 //       A^{-1} b = Vx [ (Vx^T B Vy) / (lx_i + ly_j) ] Vy^T,
-//   four dense GEMMs (cuBLAS DGEMM, FP64 tensor cores) and one scale kernel.
+//   four dense GEMMs on the FP64 tensor cores (k_dgemm_nn, hpg_gemm.cuh; the
+//   scaling fused into the second GEMM's epilogue).
 // * The SchurOperator.matvec combine (linalg.py:223-229):
 //       y = -((D x + E x) + B^T A^{-1} B x / alpha),
 //   E = beta diag(mass_psi) (obstacle, assembly.py:570-575) or
@@ -16,11 +17,6 @@
 #include "hpg_precond.cuh"
 
 namespace hpg {
-
-__global__ void k_fdm_scale(double* __restrict__ t, const double* __restrict__ finv, long long n) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    t[i] *= finv[i];
-}
 
 // y = -((yD + E x) + z / alpha) over the global psi vector
 __global__ void k_schur_combine(ElemArgs A, int gradient, double alpha, double beta, const double* __restrict__ x,

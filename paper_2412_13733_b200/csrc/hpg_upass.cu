@@ -224,16 +224,23 @@ template <int P, bool G>
 int go(const ElemArgs& A, cudaStream_t s) {
   using U = UPass<P>;
   constexpr size_t smem = sizeof(double) * (size_t)UPW * upass_bufs<G>() * U::M * U::LD;
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_upass<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_upass)", e);
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_upass<P, G>, 32 * UPW, smem);
-    grid_cap = nsm * (occ > 0 ? occ : 1);
-  }
+  struct Memo { int grid_cap = 0; };
+  static PerDevice<Memo> memo;
+  int grid_cap = 0;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if (m.grid_cap == 0) {
+      cudaError_t e = cudaFuncSetAttribute(k_upass<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      int dev = 0, nsm = 0, occ = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_upass<P, G>, 32 * UPW, smem);
+      m.grid_cap = nsm * (occ > 0 ? occ : 1);
+    }
+    grid_cap = m.grid_cap;
+    return cudaSuccess;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_upass)", se);
   int need = (A.N + UPW - 1) / UPW;
   cudaError_t e = launch_pdl(k_upass<P, G>, dim3(need < grid_cap ? need : grid_cap), dim3(32 * UPW), smem, s, A);
   if (e == cudaSuccess) e = cudaGetLastError();

@@ -69,12 +69,15 @@ template <int P, bool G>
 int go(const ElemArgs& A, cudaStream_t s) {
   constexpr int M = P + 1, N = G ? P : P - 1, NC = G ? 2 : 1;
   constexpr size_t smem = sizeof(double) * (size_t)(M * M + NC * N * N) * USM_TH;
-  static bool init = false;
-  if (!init) {
+  struct Memo { bool init = false; };
+  static PerDevice<Memo> memo;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if (m.init) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(k_usmall<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_usmall)", e);
-    init = true;
-  }
+    m.init = e == cudaSuccess;
+    return e;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_usmall)", se);
   cudaError_t e = launch_pdl(k_usmall<P, G>, dim3((A.N + USM_TH - 1) / USM_TH), dim3(USM_TH), smem, s, A);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_usmall launch", e);

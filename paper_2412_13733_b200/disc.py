@@ -325,7 +325,10 @@ class _DeviceDisc:
 
     def assemble_D_t(self, psi_t):
         clamped = self._weights_t(psi_t)
-        return DeviceCellBlockMatrix(self, self._wcache.clone(), clamped)
+        # snapshots: later residual / moments calls overwrite the disc's
+        # weight cache and clamp flag
+        return DeviceCellBlockMatrix(self, self._wcache.clone(),
+                                     clamped.clone() if clamped is not None else False)
 
     # ------------------------------------------------ per-cell Schur preconditioner
     def _precond_ready(self):

@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .disc import F64, _stream, _vp
-from .schur import gmres_t, legendre_map
+from .schur import DeviceGmres, legendre_map
 
 
 def u_matrices_full_1d(widths, p):
@@ -110,15 +110,21 @@ class DeviceTemperatureSolver:
                   _stream())
         return out
 
-    def precond_t(self, b_t):
+    def precond_t(self, b_t, out=None):
         """``H^{-1} b`` (the reference's ``splu(H).solve``)."""
         d = self.disc
-        out = torch.empty(self.nfull, dtype=F64, device=d.device)
+        out = torch.empty(self.nfull, dtype=F64, device=d.device) if out is None else out
         _lib.call("hpgUFullSolve", d.plan.handle, _vp(b_t), _vp(out), _stream())
         return out
 
     def _host_map(self, fn, vals_t):
         return torch.from_numpy(np.ascontiguousarray(fn(vals_t.cpu().numpy()), dtype=np.float64)).to(vals_t.device)
+
+    def _gmres(self):
+        """One device GMRES workspace per solver (the reference's default maxiter, linalg.py:135)."""
+        if getattr(self, "_gm", None) is None:
+            self._gm = DeviceGmres(self.nfull, 150, self.disc.device)
+        return self._gm
 
     def _residual_t(self, T, u_vals):
         gap = self.phi0_vals + self.xi_vals * self.values_t(T) - u_vals
@@ -140,10 +146,10 @@ class DeviceTemperatureSolver:
         while float(torch.linalg.vector_norm(r)) > target and newton < self.newton_maxit:
             gp = self._host_map(self.data.g_deriv, gap) * self.xi_vals
 
-            def jmul(v, gp=gp):
-                return self.operator_t(v, gp)
+            def jmul(v, out, gp=gp):
+                return self.operator_t(v, gp, out=out)
 
-            res = gmres_t(jmul, r, M=self.precond_t, side="left", rtol=self.gmres_rtol, atol=0.0)
+            res = self._gmres().solve(jmul, r, M=self.precond_t, side="left", rtol=self.gmres_rtol, atol=0.0)
             T = T - res.x
             gmres_its.append(res.iterations)
             newton += 1

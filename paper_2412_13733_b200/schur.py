@@ -10,10 +10,16 @@ Mirrors ``hpgalerkin/linalg.py``:
   GEMMs on the device (``hpgStiffnessSolve``).
 * ``DeviceSchurOperator``    -- ``SchurOperator`` (``linalg.py:213-243``):
   ``-(D + E + B^T (alpha A)^{-1} B) x`` in one C-ABI call (``hpgSchurApply``).
-* ``gmres_t``                -- ``gmres`` (``linalg.py:134-207``): unrestarted
-  GMRES with modified Gram-Schmidt and Givens rotations, same algorithm and
-  stopping rule, vectors resident on the device.
+* ``DeviceGmres`` / ``gmres_t`` -- ``gmres`` (``linalg.py:134-207``): the
+  whole unrestarted, Givens-rotated iteration on the GPU as ONE CUDA graph
+  with a device-side while loop (``hpgGmresSolve``, ``csrc/hpg_krylov.cu``):
+  CGS2 Arnoldi, rotations, residual and stopping test on the device, the
+  caller's operator kernels captured into the loop body; the reference's
+  stopping rule and result fields.
 * ``schur_solve``            -- ``schur_solve`` (``linalg.py:269-287``).
+
+Every vector operation of the solve runs in the library's own kernels
+(``hpgAxpby``, the stiffness solve's DMMA GEMMs): no cuBLAS, no ATen kernels.
 """
 
 import ctypes
@@ -142,88 +148,119 @@ class DeviceSchurOperator:
         return self.matvec(x)
 
 
-def gmres_t(amul, b, M=None, side="right", x0=None, rtol=1e-8, atol=0.0, maxiter=150):
-    """``linalg.gmres`` (``linalg.py:134-207``) on device vectors.
+def axpby_t(a, x, b, y, out):
+    """out = a x + b y on device vectors (``hpgAxpby``)."""
+    _lib.call("hpgAxpby", out.numel(), float(a), _vp(x), float(b), _vp(y), _vp(out), _stream())
+    return out
 
-    ``amul`` / ``M``: callables on device tensors.  The Hessenberg matrix,
-    rotations and the small triangular solve stay on the host (as in the
-    reference); the Krylov basis, matvecs and orthogonalisation run on the
-    GPU.  Returns ``GmresResult(x_t, iterations, residuals, converged)``.
+
+class DeviceGmres:
+    """``linalg.gmres`` (``linalg.py:134-207``) on the GPU for vectors of length n.
+
+    ``solve(amul, b, M, side, x0, rtol, atol)``: ``amul(x, out)`` and
+    ``M(x, out)`` enqueue device kernels writing ``out`` (no synchronisation,
+    no allocation: they are captured into the loop body).  Returns the
+    reference's ``GmresResult(x, iterations, residuals, converged)`` with x a
+    device tensor; one host synchronisation per solve (the status read).
     """
-    pmul = (lambda v: v) if M is None else M
-    n = b.numel()
-    x = torch.zeros(n, dtype=F64, device=b.device) if x0 is None else x0.clone()
-    if side not in ("left", "right"):
-        raise ValueError("side must be 'left' or 'right'")
-    r = b - amul(x) if bool(torch.any(x != 0)) else b.clone()
-    if side == "left":
-        r = pmul(r)
-    beta = float(torch.linalg.vector_norm(r))
-    residuals = [beta]
-    if beta == 0.0:
-        return GmresResult(x, 0, residuals, True)
-    target = max(rtol * beta, atol)
-    V = torch.empty((maxiter + 1, n), dtype=F64, device=b.device)
-    V[0] = r / beta
-    H = np.zeros((maxiter + 1, maxiter))
-    cs = np.zeros(maxiter)
-    sn = np.zeros(maxiter)
-    g = np.zeros(maxiter + 1)
-    g[0] = beta
-    converged = False
-    k = 0
-    for j in range(maxiter):
-        w = pmul(amul(V[j])) if side == "left" else amul(pmul(V[j]))
-        hs = []
-        for i in range(j + 1):                    # modified Gram-Schmidt
-            h = torch.dot(V[i], w)
-            w = w - h * V[i]
-            hs.append(h)
-        hs.append(torch.linalg.vector_norm(w))
-        col = torch.stack(hs).cpu().numpy()
-        H[: j + 2, j] = col
-        for i in range(j):
-            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-            H[i, j] = t
-        denom = np.hypot(H[j, j], H[j + 1, j])
-        if denom == 0.0:
-            cs[j], sn[j] = 1.0, 0.0
-        else:
-            cs[j] = H[j, j] / denom
-            sn[j] = H[j + 1, j] / denom
-        happy = H[j + 1, j] <= 1e-14 * max(1.0, abs(H[j, j]))
-        H[j, j] = cs[j] * H[j, j] + sn[j] * H[j + 1, j]
-        g[j + 1] = -sn[j] * g[j]
-        g[j] = cs[j] * g[j]
-        H[j + 1, j] = 0.0
-        k = j + 1
-        residuals.append(abs(g[j + 1]))
-        if residuals[-1] <= target or happy:
-            converged = True
-            break
-        V[j + 1] = w / col[-1]
-    y = sla.solve_triangular(H[:k, :k], g[:k], lower=False)
-    dx = torch.from_numpy(y).to(b.device) @ V[:k]
-    if side == "right":
-        dx = pmul(dx)
-    x = x + dx
-    if not converged and residuals[-1] <= target:
-        converged = True
-    return GmresResult(x, k, residuals, converged)
+
+    def __init__(self, n, maxiter, device):
+        self.n, self.maxiter, self.device = int(n), int(maxiter), device
+        h = ctypes.c_void_p()
+        _lib.call("hpgGmresCreate", ctypes.byref(h), self.n, self.maxiter)
+        self.handle = h
+        mk = lambda: torch.zeros(self.n, dtype=F64, device=device)
+        self.r, self.vin, self.z, self.w, self.dx = mk(), mk(), mk(), mk(), mk()
+        _lib.call("hpgGmresBind", h, _vp(self.r), _vp(self.vin), _vp(self.w))
+        self.stream = torch.cuda.Stream(device=device)     # captured: never the legacy stream
+        self._lib = _lib.load()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.hpgGmresDestroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def solve(self, amul, b, M=None, side="right", x0=None, rtol=1e-8, atol=0.0):
+        if side not in ("left", "right"):
+            raise ValueError("side must be 'left' or 'right'")
+        if b.numel() != self.n:
+            raise ValueError(f"b has {b.numel()} entries, expected {self.n}")
+        cur = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cur)
+        with torch.cuda.stream(self.stream):
+            # initial residual (linalg.py:149-152); A 0 = 0, so x0 = 0 gives r = b exactly
+            if x0 is None:
+                axpby_t(1.0, b, 0.0, None, self.r)
+            else:
+                amul(x0, self.w)
+                axpby_t(1.0, b, -1.0, self.w, self.r)
+            if side == "left" and M is not None:
+                M(self.r, self.z)
+                axpby_t(1.0, self.z, 0.0, None, self.r)
+            s = _stream()
+            _lib.call("hpgGmresCaptureBegin", self.handle, s)
+            try:
+                if M is None:
+                    amul(self.vin, self.w)
+                elif side == "right":
+                    M(self.vin, self.z)
+                    amul(self.z, self.w)
+                else:
+                    amul(self.vin, self.z)
+                    M(self.z, self.w)
+            finally:
+                _lib.call("hpgGmresCaptureEnd", self.handle, s)
+            _lib.call("hpgGmresSolve", self.handle, float(rtol), float(atol), _vp(self.dx), s)
+            it, conv = ctypes.c_int(), ctypes.c_int()
+            res = np.empty(self.maxiter + 1)
+            _lib.call("hpgGmresStatus", self.handle, ctypes.byref(it), ctypes.byref(conv),
+                      res.ctypes.data_as(ctypes.c_void_p), s)
+            k = it.value
+            x = torch.empty(self.n, dtype=F64, device=self.device)
+            dx = self.dx
+            if side == "right" and M is not None and k > 0:
+                M(self.dx, self.z)
+                dx = self.z
+            if x0 is None:
+                axpby_t(1.0, dx, 0.0, None, x)
+            else:
+                axpby_t(1.0, x0, 1.0, dx, x)
+        cur.wait_stream(self.stream)
+        return GmresResult(x, k, res[:k + 1].tolist(), bool(conv.value))
+
+
+def gmres_t(amul, b, M=None, side="right", x0=None, rtol=1e-8, atol=0.0, maxiter=150):
+    """One-shot ``DeviceGmres(...).solve`` (``linalg.gmres`` signature, device vectors)."""
+    return DeviceGmres(b.numel(), maxiter, b.device).solve(amul, b, M, side, x0, rtol, atol)
 
 
 def schur_solve_t(disc, D, alpha, beta, b_u, b_psi, A_factor=None, rtol=1e-8, atol=0.0, maxiter=150,
-                  side="right", precond=None):
-    """``linalg.schur_solve`` (``linalg.py:269-287``) on device tensors."""
+                  side="right", precond=None, gmres=None):
+    """``linalg.schur_solve`` (``linalg.py:269-287``) on device tensors.
+
+    ``gmres``: a reusable ``DeviceGmres`` for ``disc.ndof_psi`` unknowns."""
     A_factor = A_factor if A_factor is not None else DeviceStiffnessFactor(disc)
     S = DeviceSchurOperator(disc, D, beta, alpha, A_factor)
-    y = b_psi - disc.BT_u_t(A_factor.solve_t(b_u)) / alpha
+    # y = b_psi - B^T A^{-1} b_u / alpha
+    y = disc.BT_u_t(A_factor.solve_t(b_u))
+    axpby_t(1.0, b_psi, -1.0 / alpha, y, y)
     if precond is None:
         precond = disc.schur_preconditioner(D, alpha, beta)
-    res = gmres_t(S.matvec_t, y, M=precond.apply_t, side=side, rtol=rtol, atol=atol, maxiter=maxiter)
+    g = gmres if gmres is not None else DeviceGmres(disc.ndof_psi, maxiter, disc.device)
+    if g.maxiter != maxiter:
+        raise ValueError("gmres workspace was built for another maxiter")
+    res = g.solve(lambda x, out: S.matvec_t(x, out=out), y, M=lambda x, out: precond.apply_t(x, out=out),
+                  side=side, rtol=rtol, atol=atol)
     dpsi = res.x
-    du = A_factor.solve_t(b_u - disc.B_psi_t(dpsi)) / alpha
+    # du = A^{-1} (b_u - B dpsi) / alpha
+    t = disc.B_psi_t(dpsi)
+    axpby_t(1.0, b_u, -1.0, t, t)
+    du = A_factor.solve_t(t)
+    axpby_t(1.0 / alpha, du, 0.0, None, du)
     return SchurSolveResult(du, dpsi, res)
 
 

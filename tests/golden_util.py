@@ -39,6 +39,8 @@ def load_solve(name):
         d[k] = float(d[k])
     d["line_search"] = bool(d["line_search"])
     d["converged"] = bool(d["converged"])
+    d["alpha0"] = float(d["alpha"])
+    d["linear_solver"] = str(d["linear_solver"]) if "linear_solver" in d else "schur"
     return d
 
 

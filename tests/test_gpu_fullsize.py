@@ -1,6 +1,10 @@
 """GPU parity at BASELINE.json's full sizes against the (golden-pinned) CPU
 oracle, plus size-independent properties:
-* c1/c2/c3/c4 residual and Jacobian apply vs the oracle on the full meshes;
+* all 14 (config, rule) pairs: residual, Jacobian apply from psi, cached
+  apply and the fused residual + apply vs the oracle on the full meshes;
+* element blocks on the full meshes (every cell assembled in one call, the
+  multi-wave grids included), sampled cells vs the oracle's per-cell
+  weighted blocks, and the dense-block matvec vs the matrix-free apply;
 * D(psi) x three ways (matrix-free from psi, from cached weights, dense blocks);
 * exact u-side couplings (B^T u, B psi, A u) on their own;
 * linearity of the Jacobian apply in x;
@@ -34,9 +38,11 @@ def build(cfg_name, rule="gauss", ncells=None):
     return cfg, d, P, inp, dev
 
 
-@pytest.mark.parametrize("cfg_name,rule", [("c1", "gauss"), ("c1", "reference"), ("c2", "gauss"),
-                                           ("c3", "gauss"), ("c3", "reference"), ("c4p2", "gauss"),
-                                           ("c4p4", "reference"), ("c4p6", "gauss")])
+# every BASELINE.json config under both quadrature rules (14 pairs)
+ALL_PAIRS = [(c, r) for c in ("c0", "c1", "c2", "c3", "c4p2", "c4p4", "c4p6") for r in ("gauss", "reference")]
+
+
+@pytest.mark.parametrize("cfg_name,rule", ALL_PAIRS)
 def test_full_size_residual_and_apply(cfg_name, rule):
     cfg, d, P, inp, dev = build(cfg_name, rule)
     alpha = cfg.alphas[-1]
@@ -140,3 +146,53 @@ def test_cellwise_data_and_moments_from_values():
     grids = d.quad_grids()
     samples = [phi(*np.meshgrid(gx, gy, indexing="ij")) for gx, gy in grids]
     assert orc.rel_err(d.moments_from_values(samples), P.data_moments(P.sample(phi))) < TOL
+
+
+def _sample_cells(N, seed=0):
+    rng = np.random.default_rng(seed)
+    pick = {0, N - 1, N // 2, N // 3}
+    while len(pick) < min(N, 8):
+        pick.add(int(rng.integers(N)))
+    return sorted(pick)
+
+
+def _oracle_cell_block(cfg, P, inp, phi_vals, e):
+    """The oracle's weighted block(s) of cell e (assembly.py:257-263, 550-557, 804-815)."""
+    cx, cy = divmod(e, P.ncy)
+    sl = (slice(cx, cx + 1), slice(cy, cy + 1))
+    args = (P.t.S, P.t.T, P.wx[cx:cx + 1], P.wy[cy:cy + 1])
+    if cfg.kind == "obstacle":
+        tiles = P._tiles(inp["psi"])[sl]
+        W, _ = orc.clamped_exp_neg(orc.synthesize(P.t.S, tiles))
+        return orc.weighted_blocks(*args, W)[0]
+    vx = orc.synthesize(P.t.S, P._tiles(inp["psi"], 0)[sl])
+    vy = orc.synthesize(P.t.S, P._tiles(inp["psi"], 1)[sl])
+    ph = phi_vals[sl]
+    r2 = 1.0 + vx * vx + vy * vy
+    inv, inv3 = r2 ** -0.5, r2 ** -1.5
+    kxx, kxy, kyy = ph * (inv - vx * vx * inv3), ph * (-vx * vy * inv3), ph * (inv - vy * vy * inv3)
+    Wxx, Wxy, Wyy = (orc.weighted_blocks(*args, k)[0] for k in (kxx, kxy, kyy))
+    return np.block([[Wxx, Wxy], [Wxy, Wyy]])
+
+
+@pytest.mark.parametrize("cfg_name,rule", ALL_PAIRS)
+def test_full_size_blocks_sampled(cfg_name, rule):
+    """Every cell's block in ONE assembly call on the full BASELINE mesh (c1:
+    4096 cells through the persistent multi-wave block-row grid; c3: the
+    two-GEMM path), sampled cells vs the oracle at 1e-12, and the dense-block
+    matvec == the matrix-free cached apply on the whole mesh."""
+    import torch
+    cfg, d, P, inp, dev = build(cfg_name, rule)
+    phi_vals = P.sample(inp["phi"])
+    D = d.assemble_D_t(dev["psi"])
+    blocks = D.blocks_t()
+    torch.cuda.synchronize()
+    for e in _sample_cells(d.plan.ncells):
+        got = blocks[e].cpu().numpy()
+        ref = _oracle_cell_block(cfg, P, inp, phi_vals, e)
+        assert orc.rel_err(got, ref) < TOL, f"cell {e}"
+    y_blk = D.matvec_blocks_t(dev["x"]).cpu().numpy()
+    y_mf = D.matvec_t(dev["x"]).cpu().numpy()
+    assert orc.rel_err(y_blk, y_mf) < TOL
+    del blocks, D
+    torch.cuda.empty_cache()
