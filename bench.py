@@ -383,6 +383,10 @@ def schur_timing(disc, cfg, psi_prev, u, psi, b_u, b_psi, flag):
                     "schur.schur_solve_t (device GMRES graph + hpgLUSolve), preconditioner factor excluded"}
 
 
+def dist_rank():
+    return int(os.environ.get("RANK", "0"))
+
+
 def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
     """Device-timed measurement of one config; ``full`` adds the headline-only
     extras (preconditioner, Schur solve)."""
@@ -395,8 +399,26 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
     from paper_2412_13733_b200.proximal import residual
 
     nq = cfg.nq(rule)
-    inp = config_inputs(cfg, seed=0)
-    mesh = uniform_mesh_2d(0.0, 1.0, cfg.ncells, cfg.p)
+    halo = None
+    if world > 1:
+        # §8e weak scaling: ONE mesh of world x ncells cell columns, each rank
+        # owning ncells columns (its config-sized share) and running the
+        # unchanged single-GPU path on its slab + two ghost columns per
+        # interior side; ghost rows of psi, psi_prev and u come from the
+        # neighbours over NCCL at the start of every step (dist.SlabHalo)
+        from paper_2412_13733_b200.mesh import Mesh1D, TensorMesh2D
+        from paper_2412_13733_b200.workloads import make_inputs
+        rank = dist_rank()
+        halo = hdist.SlabHalo(world * cfg.ncells, cfg.ncells, cfg.p, cfg.kind, world, rank)
+        xg = np.linspace(0.0, float(world), world * cfg.ncells + 1)
+        mesh = TensorMesh2D(Mesh1D(halo.local_points(xg), np.full(halo.ncx_local, cfg.p)),
+                            Mesh1D(np.linspace(0.0, 1.0, cfg.ncells + 1), np.full(cfg.ncells, cfg.p)))
+        inp = config_inputs(cfg, seed=0)
+        psi_l, u_l, x_l, _ = make_inputs(cfg.kind, halo.ncx_local, cfg.ncells, cfg.p, seed=rank)
+        inp.update(psi=psi_l, u=u_l, x=x_l, psi_prev=np.zeros_like(psi_l))
+    else:
+        inp = config_inputs(cfg, seed=0)
+        mesh = uniform_mesh_2d(0.0, 1.0, cfg.ncells, cfg.p)
     cls = D.ObstacleDisc2D if cfg.kind == "obstacle" else D.GradientDisc2D
     disc = cls(mesh, inp["f"], inp["phi"], rule=rule, nq=nq if rule == "gauss" else None)
     dev = disc.device
@@ -469,6 +491,8 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
             flush.fill_(float(s))                  # evict L2 between steps
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(stream)
+            if halo is not None:
+                halo.exchange(psi_like=[s0["psi"], s0["psi_prev"]], u_like=[s0["u"]])
             g_res[a].replay()
             e1.record(stream)
             if g_mv is not None:
@@ -675,7 +699,9 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inputs with the config's shapes and value laws, SURVEY.md §8d)",
             "config": head["config"],
-            "parallelism": "replicas" if world > 1 else "single GPU",
+            "parallelism": (f"dp{world}: one mesh of {world}x{cfg.ncells} cell columns sharded into "
+                            f"slabs, 2 ghost columns per interface, NCCL halo exchange of psi/psi_prev/u "
+                            f"rows per step" if world > 1 else "single GPU"),
             "roofline": head["roofline"],
             "step_roofline_frac": head["step_roofline_frac"],
             "precond": head.get("precond"),

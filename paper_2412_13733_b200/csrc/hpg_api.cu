@@ -228,6 +228,7 @@ const char* hpgLastError(void) { return g_err.c_str(); }
 int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, const double* S,
                   const double* T, const double* Su, const double* Tu, const double* hx,
                   const double* hy) {
+  HPG_NVTX("hpgPlanCreate");
   if (plan == nullptr) return fail(HPG_ERR_ARG, "null plan pointer");
   *plan = nullptr;
   if (kind != HPG_OBSTACLE && kind != HPG_GRADIENT) return fail(HPG_ERR_ARG, "unknown kind");
@@ -344,6 +345,7 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
 }
 
 int hpgPlanDestroy(hpgPlan P) {
+  HPG_NVTX("hpgPlanDestroy");
   if (P == nullptr) return HPG_OK;
   cudaFree(P->Sf); cudaFree(P->Tf); cudaFree(P->hx); cudaFree(P->hy); cudaFree(P->G);
   cudaFree(P->Tuf); cudaFree(P->Suf); cudaFree(P->scratch_u); cudaFree(P->mu);
@@ -359,6 +361,7 @@ int hpgPlanDestroy(hpgPlan P) {
 }
 
 int hpgPlanInfo(hpgPlan P, long long* info) {
+  HPG_NVTX("hpgPlanInfo");
   if (int rc = check(P)) return rc;
   int nw = P->kind == HPG_OBSTACLE ? 1 : 3;
   info[0] = P->n;
@@ -379,6 +382,7 @@ int hpgPlanInfo(hpgPlan P, long long* info) {
 }
 
 int hpgObstacleMoments(hpgPlan P, const double* psi, double* out, int* clamped, double* wcache, void* stream) {
+  HPG_NVTX("hpgObstacleMoments");
   if (int rc = check(P)) return rc;
   if (P->kind != HPG_OBSTACLE) return fail(HPG_ERR_ARG, "plan is not an obstacle plan");
   if (!psi || !out || !clamped) return fail(HPG_ERR_ARG, "null pointer");
@@ -389,6 +393,7 @@ int hpgObstacleMoments(hpgPlan P, const double* psi, double* out, int* clamped, 
 }
 
 int hpgObstacleApplyD(hpgPlan P, const double* psi, const double* x, double* y, void* stream) {
+  HPG_NVTX("hpgObstacleApplyD");
   if (int rc = check(P)) return rc;
   if (P->kind != HPG_OBSTACLE) return fail(HPG_ERR_ARG, "plan is not an obstacle plan");
   if (!psi || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
@@ -402,6 +407,7 @@ int hpgObstacleApplyD(hpgPlan P, const double* psi, const double* x, double* y, 
 }
 
 int hpgGradientMoments(hpgPlan P, const double* psi, const double* phi, double* out, double* wcache, void* stream) {
+  HPG_NVTX("hpgGradientMoments");
   if (int rc = check(P)) return rc;
   if (P->kind != HPG_GRADIENT) return fail(HPG_ERR_ARG, "plan is not a gradient plan");
   if (!psi || !phi || !out) return fail(HPG_ERR_ARG, "null pointer");
@@ -411,6 +417,7 @@ int hpgGradientMoments(hpgPlan P, const double* psi, const double* phi, double* 
 }
 
 int hpgGradientApplyD(hpgPlan P, const double* psi, const double* phi, const double* x, double* y, void* stream) {
+  HPG_NVTX("hpgGradientApplyD");
   if (int rc = check(P)) return rc;
   if (P->kind != HPG_GRADIENT) return fail(HPG_ERR_ARG, "plan is not a gradient plan");
   if (!psi || !phi || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
@@ -420,6 +427,7 @@ int hpgGradientApplyD(hpgPlan P, const double* psi, const double* phi, const dou
 }
 
 int hpgApplyCached(hpgPlan P, const double* wcache, const double* x, double* y, void* stream) {
+  HPG_NVTX("hpgApplyCached");
   if (int rc = check(P)) return rc;
   if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
@@ -525,6 +533,7 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
 int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u, const double* psi,
                 const double* phi, const double* f_load, double* b_u, double* b_psi, int* clamped,
                 double* wcache, void* stream) {
+  HPG_NVTX("hpgResidual");
   return residual_impl(P, alpha, psi_prev, u, psi, phi, f_load, b_u, b_psi, clamped, wcache, nullptr,
                        nullptr, stream);
 }
@@ -532,6 +541,7 @@ int hpgResidual(hpgPlan P, double alpha, const double* psi_prev, const double* u
 int hpgResidualApply(hpgPlan P, double alpha, const double* psi_prev, const double* u, const double* psi,
                      const double* phi, const double* f_load, const double* x, double* b_u,
                      double* b_psi, double* y, int* clamped, void* stream) {
+  HPG_NVTX("hpgResidualApply");
   if (!x || !y) return fail(HPG_ERR_ARG, "null pointer");
   return residual_impl(P, alpha, psi_prev, u, psi, phi, f_load, b_u, b_psi, clamped, nullptr, x, y,
                        stream);
@@ -631,15 +641,18 @@ static int blocks_impl(hpgPlan P, const double* wcache, double* blocks, int c0, 
 }
 
 int hpgBlocks(hpgPlan P, const double* wcache, double* blocks, int c0, int count, void* stream) {
+  HPG_NVTX("hpgBlocks");
   return blocks_impl(P, wcache, blocks, c0, count, stream, 0, 1.0, 0.0);
 }
 
 int hpgPrecondAssemble(hpgPlan P, const double* wcache, double alpha, double beta, double* blocks, int c0,
                        int count, void* stream) {
+  HPG_NVTX("hpgPrecondAssemble");
   return blocks_impl(P, wcache, blocks, c0, count, stream, 1, alpha, beta);
 }
 
 int hpgBlocksMatvec(hpgPlan P, const double* blocks, const double* x, double* y, void* stream) {
+  HPG_NVTX("hpgBlocksMatvec");
   if (int rc = check(P)) return rc;
   if (!blocks || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
@@ -654,6 +667,7 @@ int hpgBlocksMatvec(hpgPlan P, const double* blocks, const double* x, double* y,
 }
 
 int hpgBTu(hpgPlan P, const double* u, double* out, void* stream) {
+  HPG_NVTX("hpgBTu");
   if (int rc = check(P)) return rc;
   if ((!u && P->ndof_u > 0) || !out) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
@@ -665,6 +679,7 @@ int hpgBTu(hpgPlan P, const double* u, double* out, void* stream) {
 }
 
 int hpgBPsi(hpgPlan P, const double* psi, double* out, void* stream) {
+  HPG_NVTX("hpgBPsi");
   if (int rc = check(P)) return rc;
   if (P->ndof_u == 0) return HPG_OK;
   if (!psi || !out) return fail(HPG_ERR_ARG, "null pointer");
@@ -674,6 +689,7 @@ int hpgBPsi(hpgPlan P, const double* psi, double* out, void* stream) {
 }
 
 int hpgAu(hpgPlan P, const double* u, double* out, void* stream) {
+  HPG_NVTX("hpgAu");
   if (int rc = check(P)) return rc;
   if (P->ndof_u == 0) return HPG_OK;
   if (!u || !out) return fail(HPG_ERR_ARG, "null pointer");
@@ -683,6 +699,7 @@ int hpgAu(hpgPlan P, const double* u, double* out, void* stream) {
 }
 
 int hpgMomentsFromValues(hpgPlan P, const double* vals, double* out, void* stream) {
+  HPG_NVTX("hpgMomentsFromValues");
   if (int rc = check(P)) return rc;
   if (!vals || !out) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
@@ -692,6 +709,7 @@ int hpgMomentsFromValues(hpgPlan P, const double* vals, double* out, void* strea
 }
 
 int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
+  HPG_NVTX("hpgLoadVector");
   if (int rc = check(P)) return rc;
   if (P->ndof_u == 0) return HPG_OK;
   if (!vals || !out) return fail(HPG_ERR_ARG, "null pointer");
@@ -714,6 +732,7 @@ int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
 // Per-cell Schur preconditioner (assembly.py:577-603, 851-860; linalg.py:246-266)
 
 int hpgPrecondPrepare(hpgPlan P, const double* Zhat, const double* lam_hat, void* stream) {
+  HPG_NVTX("hpgPrecondPrepare");
   if (int rc = check(P)) return rc;
   if (P->kind != HPG_OBSTACLE) return HPG_OK;   // the gradient blocks need no triple
   if (!Zhat || !lam_hat) return fail(HPG_ERR_ARG, "null triple factors");
@@ -777,6 +796,7 @@ static int prec_args(hpgPlan P, double* blocks, int* ipiv, int* perm, int* info,
 }
 
 int hpgPrecondBlocks(hpgPlan P, double* blocks, double alpha, double beta, int c0, int count, void* stream) {
+  HPG_NVTX("hpgPrecondBlocks");
   if (int rc = check(P)) return rc;
   PrecArgs A;
   if (int rc = prec_args(P, blocks, nullptr, nullptr, nullptr, alpha, beta, c0, count, 1, &A)) return rc;
@@ -785,6 +805,7 @@ int hpgPrecondBlocks(hpgPlan P, double* blocks, double alpha, double beta, int c
 }
 
 int hpgLUFactor(hpgPlan P, double* blocks, int* ipiv, int* perm, int count, int* info, void* stream) {
+  HPG_NVTX("hpgLUFactor");
   if (int rc = check(P)) return rc;
   PrecArgs A;
   if (int rc = prec_args(P, blocks, ipiv, perm, info, 1.0, 0.0, 0, count, 0, &A)) return rc;
@@ -795,6 +816,7 @@ int hpgLUFactor(hpgPlan P, double* blocks, int* ipiv, int* perm, int count, int*
 
 int hpgPrecondFactor(hpgPlan P, double* blocks, int* ipiv, int* perm, double alpha, double beta, int c0,
                      int count, int* info, void* stream) {
+  HPG_NVTX("hpgPrecondFactor");
   if (int rc = check(P)) return rc;
   PrecArgs A;
   if (int rc = prec_args(P, blocks, ipiv, perm, info, alpha, beta, c0, count, 1, &A)) return rc;
@@ -805,6 +827,7 @@ int hpgPrecondFactor(hpgPlan P, double* blocks, int* ipiv, int* perm, double alp
 
 int hpgLUSolve(hpgPlan P, const double* lu, const int* ipiv, const int* perm, const double* x, double* y,
                void* stream) {
+  HPG_NVTX("hpgLUSolve");
   if (int rc = check(P)) return rc;
   if (!lu || !ipiv || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs E = base_args(P);
@@ -852,6 +875,7 @@ static int fdm_setup(hpgPlan P, int slot, int r, int c, const double* Vx, const 
 
 int hpgStiffnessFactor(hpgPlan P, const double* Vx, const double* lx, const double* Vy, const double* ly,
                        void* stream) {
+  HPG_NVTX("hpgStiffnessFactor");
   if (int rc = check(P)) return rc;
   if (!Vx || !lx || !Vy || !ly) return fail(HPG_ERR_ARG, "null eigen-factors");
   if (P->nix <= 0 || P->niy <= 0) return fail(HPG_ERR_ARG, "mesh has no interior U dofs");
@@ -897,6 +921,7 @@ static int stiffness_solve(hpgPlan P, const double* b, double* x, cudaStream_t s
 }
 
 int hpgStiffnessSolve(hpgPlan P, const double* b, double* x, void* stream) {
+  HPG_NVTX("hpgStiffnessSolve");
   if (int rc = check(P)) return rc;
   if (!P->fdm_ready) return fail(HPG_ERR_ARG, "hpgStiffnessFactor has not been called on this plan");
   if (!b || !x) return fail(HPG_ERR_ARG, "null pointer");
@@ -906,6 +931,7 @@ int hpgStiffnessSolve(hpgPlan P, const double* b, double* x, void* stream) {
 
 int hpgSchurApply(hpgPlan P, const double* wcache, double alpha, double beta, const double* x, double* y,
                   void* stream) {
+  HPG_NVTX("hpgSchurApply");
   if (int rc = check(P)) return rc;
   if (!P->fdm_ready) return fail(HPG_ERR_ARG, "hpgStiffnessFactor has not been called on this plan");
   if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
@@ -931,6 +957,7 @@ int hpgSchurApply(hpgPlan P, const double* wcache, double alpha, double beta, co
 int hpgUFullSetup(hpgPlan P, double gamma, const double* SR, const double* TR, const double* Kh,
                   const double* Mh, const double* Vx, const double* lx, const double* Vy, const double* ly,
                   void* stream) {
+  HPG_NVTX("hpgUFullSetup");
   if (int rc = check(P)) return rc;
   if (!SR || !TR || !Kh || !Mh || !Vx || !lx || !Vy || !ly) return fail(HPG_ERR_ARG, "null table");
   if (P->p < 2) return fail(HPG_ERR_UNSUPPORTED, "full-space U operators need p >= 2");
@@ -992,6 +1019,7 @@ static int q_values(hpgPlan P, const double* v, cudaStream_t s) {
 }
 
 int hpgUFullValues(hpgPlan P, const double* v, double* vals, void* stream) {
+  HPG_NVTX("hpgUFullValues");
   if (int rc = check(P)) return rc;
   if (!P->q_ready) return fail(HPG_ERR_ARG, "hpgUFullSetup has not been called on this plan");
   if (!v || !vals) return fail(HPG_ERR_ARG, "null pointer");
@@ -1003,6 +1031,7 @@ int hpgUFullValues(hpgPlan P, const double* v, double* vals, void* stream) {
 
 int hpgUFullOperator(hpgPlan P, double gamma, const double* v, const double* w, const double* rhs, double* out,
                      void* stream) {
+  HPG_NVTX("hpgUFullOperator");
   if (int rc = check(P)) return rc;
   if (!P->q_ready) return fail(HPG_ERR_ARG, "hpgUFullSetup has not been called on this plan");
   if (!out) return fail(HPG_ERR_ARG, "null pointer");
@@ -1037,6 +1066,7 @@ int hpgUFullOperator(hpgPlan P, double gamma, const double* v, const double* w, 
 }
 
 int hpgUFullSolve(hpgPlan P, const double* b, double* x, void* stream) {
+  HPG_NVTX("hpgUFullSolve");
   if (int rc = check(P)) return rc;
   if (!P->q_ready) return fail(HPG_ERR_ARG, "hpgUFullSetup has not been called on this plan");
   if (!b || !x || b == x) return fail(HPG_ERR_ARG, "bad pointers");

@@ -387,6 +387,7 @@ void release(hpgGmres G) {
 extern "C" {
 
 int hpgGmresCreate(hpgGmres* out, long long n, int maxiter) {
+  HPG_NVTX("hpgGmresCreate");
   if (!out) return kfail(HPG_ERR_ARG, "null handle pointer");
   *out = nullptr;
   if (n < 1 || maxiter < 0 || maxiter > 1000) return kfail(HPG_ERR_ARG, "need n >= 1 and 0 <= maxiter <= 1000");
@@ -440,6 +441,7 @@ int hpgGmresCreate(hpgGmres* out, long long n, int maxiter) {
 }
 
 int hpgGmresDestroy(hpgGmres G) {
+  HPG_NVTX("hpgGmresDestroy");
   if (!G) return HPG_OK;
   release(G);
   cudaFree(G->mem);
@@ -449,6 +451,7 @@ int hpgGmresDestroy(hpgGmres G) {
 }
 
 int hpgGmresBind(hpgGmres G, const double* r, double* vin, double* w) {
+  HPG_NVTX("hpgGmresBind");
   if (!G) return kfail(HPG_ERR_ARG, "null gmres handle");
   if (!r || !vin || !w) return kfail(HPG_ERR_ARG, "null vector");
   if (G->capturing) return kfail(HPG_ERR_ARG, "cannot rebind during capture");
@@ -460,6 +463,7 @@ int hpgGmresBind(hpgGmres G, const double* r, double* vin, double* w) {
 }
 
 int hpgGmresCaptureBegin(hpgGmres G, void* stream) {
+  HPG_NVTX("hpgGmresCaptureBegin");
   if (!G) return kfail(HPG_ERR_ARG, "null gmres handle");
   if (G->capturing) return kfail(HPG_ERR_ARG, "capture already in progress");
   if (!G->A.r || !G->A.vin || !G->A.w) return kfail(HPG_ERR_ARG, "hpgGmresBind has not been called");
@@ -493,6 +497,7 @@ int hpgGmresCaptureBegin(hpgGmres G, void* stream) {
 }
 
 int hpgGmresCaptureEnd(hpgGmres G, void* stream) {
+  HPG_NVTX("hpgGmresCaptureEnd");
   if (!G || !G->capturing) return kfail(HPG_ERR_ARG, "no capture in progress");
   KArgs& A = G->A;
   cudaStream_t s = (cudaStream_t)stream;
@@ -512,6 +517,7 @@ int hpgGmresCaptureEnd(hpgGmres G, void* stream) {
 }
 
 int hpgGmresSolve(hpgGmres G, double rtol, double atol, double* dx, void* stream) {
+  HPG_NVTX("hpgGmresSolve");
   if (!G || !G->exec) return kfail(HPG_ERR_ARG, "gmres loop not captured");
   if (!dx) return kfail(HPG_ERR_ARG, "null dx");
   KArgs& A = G->A;
@@ -531,6 +537,7 @@ int hpgGmresSolve(hpgGmres G, double rtol, double atol, double* dx, void* stream
 }
 
 int hpgGmresStatus(hpgGmres G, int* iters, int* converged, double* residuals, void* stream) {
+  HPG_NVTX("hpgGmresStatus");
   if (!G) return kfail(HPG_ERR_ARG, "null gmres handle");
   cudaStream_t s = (cudaStream_t)stream;
   KTRY(cudaStreamSynchronize(s));
@@ -542,6 +549,7 @@ int hpgGmresStatus(hpgGmres G, int* iters, int* converged, double* residuals, vo
 }
 
 int hpgAxpby(long long n, double a, const double* x, double b, const double* y, double* out, void* stream) {
+  HPG_NVTX("hpgAxpby");
   if (n < 0 || !out || (a != 0.0 && !x) || (b != 0.0 && !y)) return kfail(HPG_ERR_ARG, "bad axpby arguments");
   if (n == 0) return HPG_OK;
   long long blocks = (n + 255) / 256;

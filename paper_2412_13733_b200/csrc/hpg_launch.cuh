@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
+
+#include <nvtx3/nvToolsExt.h>
 #include "hpg_common.cuh"
 #include "../../include/hpg_b200.h"
 
@@ -11,6 +13,14 @@ namespace hpg {
 
 int set_error(int code, const char* where, cudaError_t e);
 int set_error_msg(int code, const char* msg);
+
+// NVTX range around every C-ABI entry point (named after it), so nsys /
+// ncu --nvtx timelines attribute kernels to the reference callable they serve.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define HPG_NVTX(name) ::hpg::NvtxRange hpg_nvtx_range_(name)
 
 // Launch-setup memo per device (function attributes and occupancy are per
 // device) behind a mutex, so plans on several devices / host threads share

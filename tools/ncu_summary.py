@@ -8,9 +8,15 @@ import subprocess
 import sys
 
 rep, title = sys.argv[1], sys.argv[2]
+pick = sys.argv[3] if len(sys.argv) > 3 else None     # regex on the kernel name (first match)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-h, u, v = rows[0], rows[1], rows[2]
+h, u = rows[0], rows[1]
+v = rows[2]
+if pick:
+    import re
+    ki = h.index("Kernel Name")
+    v = next(r for r in rows[2:] if re.search(pick, r[ki]))
 print(title)
 print("kernel:", v[h.index("Kernel Name")] if "Kernel Name" in h else "?")
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
