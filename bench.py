@@ -279,16 +279,18 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(cfg, rule):
+def config_dict(cfg, rule, cached=None):
     """The workload description shared by both arms (same config => comparable)."""
     nq = cfg.nq(rule)
-    cached = not cfg.name.startswith("c4")
+    if cached is None:
+        cached = cfg.k_mv > 1
     return {"workload": f"{cfg.name}: {cfg.kind} {cfg.ncells}x{cfg.ncells} cells, p={cfg.p}, "
                         f"{rule} rule nq={nq}, (1 residual + {cfg.k_mv} Jacobian matvecs)"
                         + (f" x {cfg.reps}" if cfg.reps > 1 else "")
                         + (f", alpha cycling {list(cfg.alphas)}" if len(cfg.alphas) > 1 else ""),
             "rule": rule, "ncells": cfg.N, "p": cfg.p, "nq": nq, "k_mv": cfg.k_mv, "reps": cfg.reps,
-            "matvec": "cached point weights" if cached else "weights recomputed from psi (fused with the residual)",
+            "matvec": ("cached point weights of D(psi)" if cached else
+                       "at the same psi, fused into the residual's pass (hpgResidualApply)"),
             "l2": ("flushed between timed steps (256 MB write); repetitions rotate over buffer sets "
                    "> 2x L2" if not cached else "flushed between timed steps (256 MB write); matvecs "
                    "rotate over 8 direction vectors"),
@@ -422,7 +424,10 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
     cls = D.ObstacleDisc2D if cfg.kind == "obstacle" else D.GradientDisc2D
     disc = cls(mesh, inp["f"], inp["phi"], rule=rule, nq=nq if rule == "gauss" else None)
     dev = disc.device
-    cached = not cfg.name.startswith("c4")
+    # the Jacobian matvecs: from the residual's cached point weights (Krylov
+    # style), or -- config 4, and k_mv = 1 plans whose hpgResidualApply fuses
+    # the apply into the residual's pass -- recomputed at the same psi
+    cached = not (cfg.name.startswith("c4") or (cfg.k_mv == 1 and disc.plan.fused_apply))
     kmv, reps = cfg.k_mv, cfg.reps
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -435,7 +440,7 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
                 "y": torch.empty(disc.ndof_psi, dtype=torch.float64, device=dev)}
 
     set_bytes = 8 * (5 * disc.ndof_psi + 2 * disc.ndof_u)
-    nsets = max(3, math.ceil(2 * L2_BYTES / set_bytes)) if not cached else 1
+    nsets = min(max(3, math.ceil(2 * L2_BYTES / set_bytes)), reps) if not cached else 1
     sets = [new_set() for _ in range(nsets)]
     s0 = sets[0]
     NX = 8
@@ -542,7 +547,7 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
                 "algorithmic_per_launch": {"flops": F_mv, "bytes": B_mv},
                 "avg_launch_us": t_kern * 1e6,
                 "timing": f"CUDA events around {KREP} back-to-back launches (graph) on the launching stream"}
-    else:
+    elif cfg.name.startswith("c4"):
         t_k = statistics.mean(res_ms) / reps * 1e-3       # fused residual + apply per rep
         bytes_ = B_res + B_mv
         achieved = bytes_ / t_k / 1e9
@@ -553,6 +558,18 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
                 "algorithmic_per_launch": {"flops": F_res + F_mv, "bytes": bytes_},
                 "avg_launch_us": t_k * 1e6,
                 "timing": f"CUDA events around the step's {reps} launches (buffer sets rotated: {nsets})"}
+    else:
+        # hpgResidualApply in one row-split pass (k_wsplit_ra) + the U side and
+        # hat gather: timed as the whole call (the kernel alone is faster)
+        t_k = statistics.mean(res_ms) * 1e-3
+        achieved = (F_res + F_mv) / t_k / 1e12
+        roof = {"kernel": "hpgResidualApply = U side + k_wsplit_ra (fused residual + apply) + hat gather",
+                "bound": "tensor", "achieved": achieved, "peak": P_FP64_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / P_FP64_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peaks_r01.json)",
+                "algorithmic_per_launch": {"flops": F_res + F_mv, "bytes": B_res + B_mv},
+                "avg_launch_us": t_k * 1e6,
+                "timing": "CUDA events around the whole call (3 kernels) on the launching stream"}
     t_lb = max((F_res + kmv * F_mv) / (P_FP64_TFLOPS * 1e12), (B_res + kmv * B_mv) / (hbm * 1e9)) * reps
     step_frac = t_lb / (statistics.mean(step_ms) * 1e-3)
 
@@ -582,7 +599,7 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
                "ms_per_step_min_median_max": [1e3 * min(t_e2e), 1e3 * statistics.median(t_e2e), 1e3 * max(t_e2e)],
                "path": "paper_2412_13733_b200.proximal.residual + disc.assemble_D + (D @ x) x k_mv, NumPy in/out"}
 
-    rec = {"config": config_dict(cfg, rule), "value": value, "ms_per_step": total_ms / args.steps,
+    rec = {"config": config_dict(cfg, rule, cached), "value": value, "ms_per_step": total_ms / args.steps,
            "roofline": roof, "step_roofline_frac": step_frac, "e2e": e2e,
            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
            "res_ms_mean": statistics.mean(res_ms), "mv_ms_mean": statistics.mean(mv_ms) if mv_ms else None,

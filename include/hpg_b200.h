@@ -64,10 +64,11 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq,
                   const double* S, const double* T, const double* Su,
                   const double* Tu, const double* hx, const double* hy);
 int hpgPlanDestroy(hpgPlan plan);
-/* info[0..10] = n, m, nq, ncells, ndof_psi, ndof_u, wcache_doubles,
- *               block_doubles_per_cell, path(0 warp, 1 cta), splits,
- *               kernels per hpgResidualApply call (1: single-pass path).
- * info must hold at least 11 entries. */
+/* info[0..11] = n, m, nq, ncells, ndof_psi, ndof_u, wcache_doubles,
+ *               block_doubles_per_cell, path(0 warp, 1 cta, 2 row-split), splits,
+ *               kernels per hpgResidualApply call (1: single-pass path),
+ *               1 if hpgResidualApply fuses the apply into the residual pass.
+ * info must hold at least 12 entries. */
 int hpgPlanInfo(hpgPlan plan, long long* info);
 
 /* ObstacleDisc2D.exp_moments (assembly.py:541-548).  out[ndof_psi].
@@ -151,7 +152,10 @@ int hpgLoadVector(hpgPlan plan, const double* vals, double* out, void* stream);
  * hpgPrecondFactor: both, fused (blocks hold D on entry, LU of P on exit).
  * hpgLUSolve: CellBlockPreconditioner.apply (linalg.py:253-257):
  * y[idx_e] = lu_solve(LU_e, x[idx_e]) for every cell (perm nullable).
- * hpgLUMaxBlock: largest block side the per-CTA factorisation supports. */
+ * hpgLUMaxBlock: largest block side the factorisation supports (one CTA per
+ * block up to ~3k, beyond that -- config 3's 6561^2 -- a blocked LU with
+ * 32-column panels held in the distributed shared memory of an 8-CTA cluster
+ * per block and batched DMMA trailing updates). */
 int hpgPrecondPrepare(hpgPlan plan, const double* Zhat, const double* lam_hat,
                       void* stream);
 int hpgPrecondBlocks(hpgPlan plan, double* blocks, double alpha, double beta,

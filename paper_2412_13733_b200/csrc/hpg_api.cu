@@ -80,7 +80,8 @@ struct hpgPlan_st {
   int NT, QT, NP, QP;
   int nix, niy;
   long long ncomp, ndof_psi, ndof_u;
-  int use_warp[8];
+  int path[8];                  // ElemPath per element-kernel mode
+  bool fused_ra = false;        // hpgResidualApply as one row-split kernel (k_wsplit_ra)
   int splits;
   double *Sf = nullptr, *Tf = nullptr, *hx = nullptr, *hy = nullptr;
   double* G = nullptr;        // block table [n2][QP]
@@ -162,8 +163,8 @@ bool warp_fits(int mode, int NT, int QT) {
 
 template <int MODE>
 int run_elem(hpgPlan_st* P, ElemArgs A, cudaStream_t s) {
-  if (!P->use_warp[MODE]) A.splits = P->splits;
-  return run_mode<MODE>(P->use_warp[MODE] != 0, A, s);
+  if (P->path[MODE] == PATH_CTA) A.splits = P->splits;
+  return run_mode<MODE>(P->path[MODE], A, s);
 }
 
 // shared memory of the block-row kernel (k_blockrow, 4 warps): PK(G) staged
@@ -187,6 +188,18 @@ size_t blockrow_smem(const hpgPlan_st* P, int* pk_smem) {
 bool blocks_use_gemm(const hpgPlan_st* P) {
   int pk;
   return blockrow_smem(P, &pk) > ((size_t)200 << 10) || P->NT > 4;
+}
+
+bool wsplit_fits(int mode, int NT, int QT) {
+  switch (mode) {
+    case M_OBST_RES: return wsplit_available<M_OBST_RES>(NT, QT);
+    case M_OBST_APPLY: return wsplit_available<M_OBST_APPLY>(NT, QT);
+    case M_OBST_CACHED: return wsplit_available<M_OBST_CACHED>(NT, QT);
+    case M_GRAD_RES: return wsplit_available<M_GRAD_RES>(NT, QT);
+    case M_GRAD_APPLY: return wsplit_available<M_GRAD_APPLY>(NT, QT);
+    case M_GRAD_CACHED: return wsplit_available<M_GRAD_CACHED>(NT, QT);
+    default: return false;
+  }
 }
 
 int check(hpgPlan p) {
@@ -307,13 +320,21 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
   if (e != cudaSuccess) { hpgPlanDestroy(P); return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
 
   // path selection
-  P->use_warp[M_OBST_RES] = warp_fits(M_OBST_RES, P->NT, P->QT);
-  P->use_warp[M_OBST_APPLY] = warp_fits(M_OBST_APPLY, P->NT, P->QT);
-  P->use_warp[M_OBST_CACHED] = warp_fits(M_OBST_CACHED, P->NT, P->QT);
-  P->use_warp[M_GRAD_RES] = warp_fits(M_GRAD_RES, P->NT, P->QT);
-  P->use_warp[M_GRAD_APPLY] = warp_fits(M_GRAD_APPLY, P->NT, P->QT);
-  P->use_warp[M_GRAD_CACHED] = warp_fits(M_GRAD_CACHED, P->NT, P->QT);
-  P->use_warp[M_VALUES] = 0;
+  // element-kernel path per mode: a warp per element when there is an
+  // instantiation and enough elements to fill the GPU; few mid-size elements
+  // (config 2: 256, config 0: 16) take a CTA per element with a warp per
+  // row tile; the rest the generic CTA path
+  {
+    const bool ws_ok = P->N < 4 * P->nsm && getenv("HPG_NO_WSPLIT") == nullptr;
+    for (int mode = M_OBST_RES; mode <= M_GRAD_CACHED; ++mode) {
+      P->path[mode] = warp_fits(mode, P->NT, P->QT) ? PATH_WARP : PATH_CTA;
+      if (ws_ok && wsplit_fits(mode, P->NT, P->QT)) P->path[mode] = PATH_WSPLIT;
+    }
+    P->path[M_VALUES] = PATH_CTA;
+    const int rmode = kind == HPG_OBSTACLE ? M_OBST_RES : M_GRAD_RES;
+    P->fused_ra = P->path[rmode] == PATH_WSPLIT && wsplit_ra_available(kind == HPG_GRADIENT, P->NT, P->QT) &&
+                  getenv("HPG_NO_FUSED_RA") == nullptr;
+  }
   // split the Q row tiles of an element across CTAs when there are few elements
   // (one wave: the largest divisor of QT with N * splits <= #SMs, so every
   // split gets the same number of row tiles)
@@ -373,11 +394,16 @@ int hpgPlanInfo(hpgPlan P, long long* info) {
   info[6] = (long long)P->N * P->QT * P->QT * nw * 64;
   long long nb = (long long)P->n * P->n * (P->kind == HPG_OBSTACLE ? 1 : 2);
   info[7] = nb * nb;
-  info[8] = P->kind == HPG_OBSTACLE ? (P->use_warp[M_OBST_RES] ? 0 : 1) : (P->use_warp[M_GRAD_RES] ? 0 : 1);
+  {
+    const int pm = P->path[P->kind == HPG_OBSTACLE ? M_OBST_RES : M_GRAD_RES];
+    info[8] = pm == PATH_WARP ? 0 : (pm == PATH_CTA ? 1 : 2);
+  }
   info[9] = P->splits;
   // kernels per fused residual + apply call: 1 on the single-pass low-degree
   // path (k_lowp), else U side + psi side + hat gather (+ apply)
   info[10] = (P->kind == HPG_OBSTACLE && P->small && lowp_available(P->p, P->nq)) ? 1 : 3;
+  // 1 when hpgResidualApply computes the apply inside the residual's pass
+  info[11] = (P->kind == HPG_OBSTACLE && P->small) || P->fused_ra ? 1 : 0;
   return HPG_OK;
 }
 
@@ -512,6 +538,13 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     // at the same psi when x is given) in a single pass over psi
     if (x != nullptr) { A.in1 = x; A.wc_out = y; }
     rc = run_small(P->n, P->nq, true, x != nullptr, A, P->stab, s);
+    x = nullptr;
+  } else if (x != nullptr && P->fused_ra) {
+    // few mid-size cells: residual + Jacobian apply in one row-split launch,
+    // D(psi)'s point weights handed over in shared memory (hpg_wsplit.cuh)
+    A.in1 = x;
+    A.wc_out = y;
+    rc = run_wsplit_ra(P->kind == HPG_GRADIENT, A, s);
     x = nullptr;
   } else {
     rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, A, s) : run_elem<M_GRAD_RES>(P, A, s);
@@ -705,7 +738,7 @@ int hpgMomentsFromValues(hpgPlan P, const double* vals, double* out, void* strea
   ElemArgs A = base_args(P);
   A.in0 = vals; A.out = out;
   A.splits = P->splits;
-  return run_mode<M_VALUES>(false, A, (cudaStream_t)stream);
+  return run_mode<M_VALUES>(PATH_CTA, A, (cudaStream_t)stream);
 }
 
 int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
@@ -721,7 +754,7 @@ int hpgLoadVector(hpgPlan P, const double* vals, double* out, void* stream) {
   A.ncomp = (long long)P->ncx * P->m * P->ncy * P->m;
   A.in0 = vals; A.out = P->mu;
   A.splits = P->splits;
-  int rc = run_mode<M_VALUES>(false, A, s);
+  int rc = run_mode<M_VALUES>(PATH_CTA, A, s);
   if (rc) return rc;
   UArgs U = base_uargs(P);
   U.mu = P->mu; U.out = out;
@@ -835,7 +868,15 @@ int hpgLUSolve(hpgPlan P, const double* lu, const int* ipiv, const int* perm, co
   return launch_lu_solve(E, lu, ipiv, perm, nb, x, y, (cudaStream_t)stream);
 }
 
-int hpgLUMaxBlock(void) { return lu_max_nb(); }
+int hpgLUMaxBlock(void) {
+  // the one-CTA panel LU up to lu_max_nb(), the cluster-panel blocked LU beyond
+  int lo = lu_max_nb(), hi = 1 << 16;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (lu_big_supported(mid)) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 
 int hpgLUProfile(unsigned long long* counters) {
   g_lu_prof = counters;

@@ -4,7 +4,8 @@
 // SURVEY.md §8f rank 4) and the QVI full-space U synthesis / analysis
 // (qvi.py:34-57, §8f rank 3).
 //
-//   C[b] = (A[b] B[b]) (.* F)         A: M x K (lda), B: K x N (ldb), C: M x N (ldc)
+//   C[b] = alpha (A[b] B[b]) (.* F) + beta C[b]
+//        A: M x K (lda), B: K x N (ldb), C: M x N (ldc)
 //
 // with batch strides (0 = operand shared by the batch) and an optional
 // elementwise epilogue factor F (M x N, ldc; the 1/(lx_i + ly_j) scaling of
@@ -32,6 +33,7 @@ struct GemmNN {
   double* C;
   const double* F;             // optional epilogue factor (stride sF, ld ldc)
   long long sF;
+  double alpha = 1.0, beta = 0.0;   // C = alpha (A B) (.* F) + beta C
 };
 
 constexpr int GM_BM = 64, GM_BN = 64, GM_BK = 16;
@@ -44,7 +46,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(sz) : "memory");
 }
 
-__global__ void __launch_bounds__(128) k_dgemm_nn(GemmNN g) {
+static __global__ void __launch_bounds__(128) k_dgemm_nn(GemmNN g) {
   __shared__ double sA[2][GM_BM * GM_LDA];
   __shared__ double sB[2][GM_BK * GM_LDB];
   const int b = blockIdx.z;
@@ -117,6 +119,8 @@ __global__ void __launch_bounds__(128) k_dgemm_nn(GemmNN g) {
         if (row < g.M && col < g.N) {
           double v = acc[i][j][q];
           if (F) v *= F[(long long)row * g.ldc + col];
+          if (g.alpha != 1.0) v *= g.alpha;
+          if (g.beta != 0.0) v += g.beta * C[(long long)row * g.ldc + col];
           C[(long long)row * g.ldc + col] = v;
         }
       }
@@ -131,6 +135,8 @@ inline cudaError_t dgemm_nn(const GemmNN& g, int batch, cudaStream_t s) {
 inline GemmNN gemm_nn(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb,
                       double* C, long long ldc) {
   GemmNN g{};
+  g.alpha = 1.0;
+  g.beta = 0.0;
   g.M = M; g.N = N; g.K = K;
   g.lda = lda; g.ldb = ldb; g.ldc = ldc;
   g.A = A; g.B = B; g.C = C;

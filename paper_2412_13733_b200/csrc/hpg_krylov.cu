@@ -431,10 +431,22 @@ int hpgGmresCreate(hpgGmres* out, long long n, int maxiter) {
   A.y = p; p += m + 2;
   A.partial = p;
   A.st = G->st;
-  if (G->smem > (48u << 10)) {
-    cudaFuncSetAttribute(k_arn_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G->smem);
-    cudaFuncSetAttribute(k_arn_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G->smem);
-    cudaFuncSetAttribute(k_arn_norm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G->smem);
+  // the attribute only grows (another solver object may need more)
+  struct Memo { size_t attr = 48u << 10; };
+  static hpg::PerDevice<Memo> memo;
+  cudaError_t ae = memo.with([&](Memo& mm) -> cudaError_t {
+    if (G->smem <= mm.attr) return cudaSuccess;
+    cudaError_t r = cudaFuncSetAttribute(k_arn_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G->smem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_arn_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G->smem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_arn_norm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G->smem);
+    if (r == cudaSuccess) mm.attr = G->smem;
+    return r;
+  });
+  if (ae != cudaSuccess) {
+    cudaFree(G->mem);
+    cudaFree(G->st);
+    delete G;
+    return kfail(HPG_ERR_CUDA, std::string("gmres smem attribute: ") + cudaGetErrorString(ae));
   }
   *out = G;
   return HPG_OK;

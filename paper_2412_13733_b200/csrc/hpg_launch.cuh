@@ -40,11 +40,21 @@ struct PerDevice {
   }
 };
 
-// Is there a warp-per-element instantiation for (NT, QT) in this mode?
+// Element-kernel paths: CTA per (element, row-tile split) (k_cta, any size),
+// warp per element (k_warp), CTA per element with a warp per row tile
+// (k_wsplit, few mid-size elements).
+enum ElemPath : int { PATH_CTA = 0, PATH_WARP = 1, PATH_WSPLIT = 2 };
+// Is there a warp-per-element / row-split instantiation for (NT, QT) in this mode?
 template <int MODE> bool warp_available(int NT, int QT);
-// Launch the element kernel of MODE (warp path if use_warp, else CTA path
-// with A.splits row-tile splits + deterministic reduction).
-template <int MODE> int run_mode(bool use_warp, ElemArgs A, cudaStream_t s);
+template <int MODE> bool wsplit_available(int NT, int QT);
+// Launch the element kernel of MODE on `path` (the CTA path runs A.splits
+// row-tile splits + a deterministic reduction).
+template <int MODE> int run_mode(int path, ElemArgs A, cudaStream_t s);
+
+// Fused residual + Jacobian apply, row-split (hpg_wsplit_ra.cu): A.out =
+// b_psi (residual combine), A.wc_out = y.
+bool wsplit_ra_available(bool gradient, int NT, int QT);
+int run_wsplit_ra(bool gradient, const ElemArgs& A, cudaStream_t s);
 
 // Thread-per-element low-degree obstacle kernel (hpg_small.cuh).
 struct SmallTables;

@@ -5,6 +5,11 @@
 #include <cstdlib>
 #include "hpg_elem.cuh"
 #include "hpg_launch.cuh"
+#include "hpg_wsplit.cuh"
+
+#ifndef HPG_WSPLIT_LIST
+#define HPG_WSPLIT_LIST
+#endif
 
 namespace hpg {
 namespace {
@@ -62,6 +67,27 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_warp launch", e);
 }
 
+template <int NT, int QT, int MODE>
+int launch_wsplit_t(const ElemArgs& A, cudaStream_t s) {
+  using CF = WsplitCfg<NT, QT, MODE>;
+  const size_t smem = sizeof(double) * (size_t)CF::SMEM_DBL;
+  if (smem > 227 * 1024) return set_error_msg(HPG_ERR_UNSUPPORTED, "row-split kernel shared memory too large");
+  struct Memo { size_t attr = 0; };
+  static PerDevice<Memo> memo;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if (smem > m.attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_wsplit<NT, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      m.attr = smem;
+    }
+    return cudaSuccess;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_wsplit)", se);
+  cudaError_t e = launch_pdl(k_wsplit<NT, QT, MODE>, dim3(A.N), dim3(32 * QT), smem, s, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_wsplit launch", e);
+}
+
 template <int MODE, int MAXS, int W>
 int launch_cta_t(ElemArgs A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
@@ -100,8 +126,11 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
     if (!try_cluster) return cudaSuccess;
     if (m.ok_splits != A.splits || m.ok_n != A.N || m.ok_np != NP) {
       m.ok_splits = A.splits; m.ok_n = A.N; m.ok_np = NP; m.ok_res = 0;
+      // (never LOWER the attribute: it must cover the largest smem launched so far)
       if (csmem <= 227 * 1024 &&
-          cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem) == cudaSuccess) {
+          ((int)csmem <= m.attr ||
+           cudaFuncSetAttribute(k_cta<MODE, MAXS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem) ==
+               cudaSuccess)) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(A.N * A.splits);
         q.blockDim = dim3(32 * W);
@@ -180,13 +209,27 @@ static int warp_dispatch(int NT, int QT, bool launch, const ElemArgs& A, cudaStr
   return launch ? set_error_msg(HPG_ERR_UNSUPPORTED, "no warp instantiation") : 0;
 }
 
+#define HPG_WS(NT_, QT_) \
+  if (NT == NT_ && QT == QT_) return launch ? launch_wsplit_t<NT_, QT_, HPG_MODE>(A, s) : 1;
+
+static int wsplit_dispatch(int NT, int QT, bool launch, const ElemArgs& A, cudaStream_t s) {
+  HPG_WSPLIT_LIST
+  return launch ? set_error_msg(HPG_ERR_UNSUPPORTED, "no row-split instantiation") : 0;
+}
+
 template <> bool warp_available<HPG_MODE>(int NT, int QT) {
   ElemArgs dummy{};
   return warp_dispatch(NT, QT, false, dummy, 0) == 1;
 }
 
-template <> int run_mode<HPG_MODE>(bool use_warp, ElemArgs A, cudaStream_t s) {
-  if (use_warp) return warp_dispatch(A.NT, A.QT, true, A, s);
+template <> bool wsplit_available<HPG_MODE>(int NT, int QT) {
+  ElemArgs dummy{};
+  return wsplit_dispatch(NT, QT, false, dummy, 0) == 1;
+}
+
+template <> int run_mode<HPG_MODE>(int path, ElemArgs A, cudaStream_t s) {
+  if (path == PATH_WARP) return warp_dispatch(A.NT, A.QT, true, A, s);
+  if (path == PATH_WSPLIT) return wsplit_dispatch(A.NT, A.QT, true, A, s);
   return launch_cta<HPG_MODE>(A, s);
 }
 

@@ -673,6 +673,16 @@ int launch_precond_transform(const PrecArgs& A, cudaStream_t s) {
 }
 
 int launch_lu(const PrecArgs& A, int nsm, cudaStream_t s) {
+  if (A.nb > lu_max_nb() && lu_big_supported(A.nb)) {
+    // blocks beyond the one-CTA panel (config 3): cluster-panel blocked LU
+    if (A.transform) {
+      int rc = launch_precond_transform(A, s);
+      if (rc) return rc;
+    }
+    PrecArgs B = A;
+    B.transform = 0;
+    return launch_lu_big(B, s);
+  }
   if (A.nb <= 8) return launch_lu_warp_t<8>(A, nsm, s);
   if (A.nb <= 16) return launch_lu_warp_t<16>(A, nsm, s);
   if (A.nb <= 32) return launch_lu_warp_t<32>(A, nsm, s);

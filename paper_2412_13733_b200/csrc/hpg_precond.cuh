@@ -77,5 +77,8 @@ int launch_lu(const PrecArgs& A, int nsm, cudaStream_t s);
 int launch_lu_solve(const ElemArgs& E, const double* lu, const int* ipiv, const int* perm, int nb,
                     const double* x, double* y, cudaStream_t s);
 int lu_max_nb();
+// blocked LU for blocks beyond lu_max_nb() (hpg_lu_big.cu)
+bool lu_big_supported(int nb);
+int launch_lu_big(const PrecArgs& A, cudaStream_t s);
 
 }  // namespace hpg

@@ -99,10 +99,14 @@ __global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG, 
   const long long base0 = psi_index(A, cx, cy, 0, 0);
   double* sC = smem + 2 * m + 8 + (size_t)(grp < cpb ? grp : 0) * (m * ld + 2 * n * n);  // m x ld U tile
   double* sG = sC + m * ld;               // [comp][n][n] weighted psi_prev - psi
+  // unrolled so every thread's gathers are in flight together (one L2 round
+  // trip per 8 entries instead of one per entry)
+#pragma unroll 8
   for (int t = valid ? t0 : m * m; t < m * m; t += TG) {
     const int i = t / m, l = t - i * m;
     sC[i * ld + l] = u_at(A, cx, cy, i, l);
   }
+#pragma unroll 8
   for (int t = valid ? t0 : n * n * 2; t < n * n * (GRADIENT ? 2 : 1); t += TG) {
     const int comp = t / (n * n), r = t - comp * n * n, i = r / n, l = r - i * n;
     const long long gi = comp * A.ncomp + base0 + (long long)i * A.ld + l;

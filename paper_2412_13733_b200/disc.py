@@ -55,11 +55,11 @@ class Plan:
         _lib.call("hpgPlanCreate", ctypes.byref(h), kind, ncx, ncy, p, tables.nq,
                   *[a.ctypes.data_as(ctypes.c_void_p) for a in arrs])
         self.handle = h
-        info = (ctypes.c_longlong * 11)()
+        info = (ctypes.c_longlong * 12)()
         _lib.call("hpgPlanInfo", h, info)
         (self.n, self.m, self.nq, self.ncells, self.ndof_psi, self.ndof_u,
          self.wcache_len, self.block_len, self.path, self.splits,
-         self.residual_apply_kernels) = [int(v) for v in info]
+         self.residual_apply_kernels, self.fused_apply) = [int(v) for v in info]
 
     def __del__(self):
         h = getattr(self, "handle", None)

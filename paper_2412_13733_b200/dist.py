@@ -188,22 +188,24 @@ class SlabHalo:
 
 
 def exchange_in_process(halos, psi_like, u_like):
-    """The same exchange between SlabHalo objects of ONE process (all ranks'
-    local tensors given as lists indexed by rank): single-GPU slab tests."""
+    """The same exchange between SlabHalo objects of ONE process: ``psi_like``
+    / ``u_like`` are lists of fields, each a list of the ranks' local tensors
+    (single-GPU slab tests)."""
     for r, h in enumerate(halos):
         for q, plan in h.peers.items():
             src = halos[q]
             mine = src.peers[r]
-            for kind, tensors in (("psi", psi_like), ("u", u_like)):
-                dst_t, src_t = tensors[r], tensors[q]
-                if kind == "psi":
-                    dv, sv, dim = h.psi_view(dst_t), src.psi_view(src_t), 1
-                else:
-                    dv, sv, dim = h.u_view(dst_t), src.u_view(src_t), 0
-                si = torch.as_tensor(mine["send_" + kind], device=sv.device)
-                ri = torch.as_tensor(plan["recv_" + kind], device=dv.device)
-                if ri.numel():
-                    dv.index_copy_(dim, ri, sv.index_select(dim, si))
+            for kind, fields in (("psi", psi_like), ("u", u_like)):
+                for per_rank in fields:
+                    dst_t, src_t = per_rank[r], per_rank[q]
+                    if kind == "psi":
+                        dv, sv, dim = h.psi_view(dst_t), src.psi_view(src_t), 1
+                    else:
+                        dv, sv, dim = h.u_view(dst_t), src.u_view(src_t), 0
+                    si = torch.as_tensor(mine["send_" + kind], device=sv.device)
+                    ri = torch.as_tensor(plan["recv_" + kind], device=dv.device)
+                    if ri.numel():
+                        dv.index_copy_(dim, ri, sv.index_select(dim, si))
 
 
 def barrier(device=None):

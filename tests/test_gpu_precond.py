@@ -31,6 +31,7 @@ def test_precond_blocks_and_apply_golden(name):
             d.schur_preconditioner(D, g["alpha"], beta)
         return
     pb = d.precond_blocks(D, g["alpha"], beta)          # fused into the blocks kernel
+    M3 = None
     if g["p"] < 82:
         # from a host CellBlockMatrix-like D (hpgPrecondBlocks transform path)
         from types import SimpleNamespace
@@ -44,8 +45,6 @@ def test_precond_blocks_and_apply_golden(name):
         assert orc.rel_err(np.stack(pb)[:, g["block_rows"], :], g["precond_sel"]) < TOL
     if not np.isfinite(g["precond_apply"]).all():
         return                                          # exactly singular (clamp case)
-    if g["kind"] == "obstacle" and g["p"] == 82:
-        return                                          # 6561^2 blocks: beyond the per-CTA LU
     M = d.schur_preconditioner(D, g["alpha"], beta)
     assert orc.rel_err(M.apply(g["x"]), g["precond_apply"]) < TOL
     assert orc.rel_err(M(g["x"]), g["precond_apply"]) < TOL
@@ -129,16 +128,33 @@ def test_full_size_preconditioner(cfg_name, rule):
     torch.cuda.synchronize()
 
 
-def test_lu_unsupported_size_is_loud():
-    """c3 (6561^2 blocks) exceeds the per-CTA LU: an error, never a CPU fallback."""
+def test_c3_blocked_lu_full_size():
+    """Config 3 at full size: 16 blocks of 6561^2 through the cluster-panel
+    blocked LU (hpg_lu_big.cu); two cells' solves against scipy's
+    lu_factor / lu_solve of the same device-built P blocks, and the pivots of
+    cell 0 against LAPACK's."""
+    import scipy.linalg as sla
+    import torch
     from paper_2412_13733_b200 import _lib
-    lib = _lib.load()
-    assert lib.hpgLUMaxBlock() < 6561
-    cfg, d, P, inp, dev = build("c3", "gauss", ncells=1)
-    d.residual_t(1.0, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
+    assert _lib.load().hpgLUMaxBlock() >= 6561
+    cfg, d, P, inp, dev = build("c3", "gauss")
+    alpha, beta = 1.0, 1e-3
+    d.residual_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], wcache=True)
     D = d.assemble_D_t(dev["psi"])
-    with pytest.raises(_lib.HpgError):
-        d.schur_preconditioner(D, 1.0, 0.0)
+    M = d.schur_preconditioner(D, alpha, beta)
+    y = M.apply_t(dev["x"]).cpu().numpy()
+    Pb = d.precond_blocks_t(D, alpha, beta)
+    piv = M.piv_t.cpu().numpy()
+    for e in (0, d.plan.ncells - 1):
+        blk = Pb[e].cpu().numpy()
+        lu, rpiv = sla.lu_factor(blk)
+        idx = d.cell_psi_indices[e]
+        ref = sla.lu_solve((lu, rpiv), inp["x"][idx])
+        assert orc.rel_err(y[idx], ref) < TOL, f"cell {e}"
+        if e == 0:
+            assert np.array_equal(piv[0], rpiv)
+    del Pb, D, M
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("kind,p", [("obstacle", 4), ("obstacle", 16), ("gradient", 6)])
