@@ -81,7 +81,16 @@ struct hpgPlan_st {
   int nix, niy;
   long long ncomp, ndof_psi, ndof_u;
   int path[8];                  // ElemPath per element-kernel mode
-  bool fused_ra = false;        // hpgResidualApply as one row-split kernel (k_wsplit_ra)
+  // few-cell plans: U side / apply concurrent with the psi side (residual_concurrent)
+  bool concurrent = false;
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  double* mscr = nullptr;       // psi-side moments [ndof_psi]
+  double* wscr = nullptr;       // weight cache of the fused residual + cached apply
+  // weight cache written by the LAST kernel of this plan's most recent call
+  // (nullptr if that kernel wrote none): the next cached apply may prefetch
+  // any other cache before its grid-dependency wait
+  const double* last_wc = nullptr;
   int splits;
   double *Sf = nullptr, *Tf = nullptr, *hx = nullptr, *hy = nullptr;
   double* G = nullptr;        // block table [n2][QP]
@@ -204,6 +213,7 @@ bool wsplit_fits(int mode, int NT, int QT) {
 
 int check(hpgPlan p) {
   if (p == nullptr) return fail(HPG_ERR_ARG, "null plan");
+  p->last_wc = nullptr;        // entry points that end with a cache writer set it again
   return HPG_OK;
 }
 
@@ -331,9 +341,21 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
       if (ws_ok && wsplit_fits(mode, P->NT, P->QT)) P->path[mode] = PATH_WSPLIT;
     }
     P->path[M_VALUES] = PATH_CTA;
-    const int rmode = kind == HPG_OBSTACLE ? M_OBST_RES : M_GRAD_RES;
-    P->fused_ra = P->path[rmode] == PATH_WSPLIT && wsplit_ra_available(kind == HPG_GRADIENT, P->NT, P->QT) &&
-                  getenv("HPG_NO_FUSED_RA") == nullptr;
+  }
+  // few cells: the U side (and the apply of hpgResidualApply) overlap the
+  // psi-side quadrature on two auxiliary streams
+  if (P->N < 4 * P->nsm && getenv("HPG_NO_CONCURRENT") == nullptr &&
+      !(kind == HPG_OBSTACLE && P->small && lowp_available(p, nq))) {
+    const size_t wlen = (size_t)P->N * P->QT * P->QT * (kind == HPG_OBSTACLE ? 1 : 3) * 64;
+    e = cudaStreamCreateWithFlags(&P->aux[0], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P->aux[1], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_join[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&P->mscr, sizeof(double) * P->ndof_psi + 16);
+    if (e == cudaSuccess) e = cudaMalloc(&P->wscr, sizeof(double) * wlen + 16);
+    if (e != cudaSuccess) { hpgPlanDestroy(P); return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
+    P->concurrent = true;
   }
   // split the Q row tiles of an element across CTAs when there are few elements
   // (one wave: the largest divisor of QT with N * splits <= #SMs, so every
@@ -377,6 +399,12 @@ int hpgPlanDestroy(hpgPlan P) {
   cudaFree(P->qSR); cudaFree(P->qTR); cudaFree(P->qK); cudaFree(P->qM); cudaFree(P->qC); cudaFree(P->qT);
   cudaFree(P->qV); cudaFree(P->qG); cudaFree(P->qP1); cudaFree(P->qP2); cudaFree(P->qH1); cudaFree(P->qH2);
   cudaFree(P->qH3); cudaFree(P->qSRT); cudaFree(P->qTRT); cudaFree(P->qKT); cudaFree(P->qMT);
+  cudaFree(P->mscr); cudaFree(P->wscr);
+  if (P->aux[0]) cudaStreamDestroy(P->aux[0]);
+  if (P->aux[1]) cudaStreamDestroy(P->aux[1]);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_join[0]) cudaEventDestroy(P->ev_join[0]);
+  if (P->ev_join[1]) cudaEventDestroy(P->ev_join[1]);
   delete P;
   return HPG_OK;
 }
@@ -403,7 +431,7 @@ int hpgPlanInfo(hpgPlan P, long long* info) {
   // path (k_lowp), else U side + psi side + hat gather (+ apply)
   info[10] = (P->kind == HPG_OBSTACLE && P->small && lowp_available(P->p, P->nq)) ? 1 : 3;
   // 1 when hpgResidualApply computes the apply inside the residual's pass
-  info[11] = (P->kind == HPG_OBSTACLE && P->small) || P->fused_ra ? 1 : 0;
+  info[11] = (P->kind == HPG_OBSTACLE && P->small) || P->concurrent ? 1 : 0;
   return HPG_OK;
 }
 
@@ -415,7 +443,9 @@ int hpgObstacleMoments(hpgPlan P, const double* psi, double* out, int* clamped, 
   ElemArgs A = base_args(P);
   A.in0 = psi; A.out = out; A.flag = clamped; A.wc_out = wcache;
   if (P->small && wcache == nullptr) return run_small(P->n, P->nq, true, false, A, P->stab, (cudaStream_t)stream);
-  return run_elem<M_OBST_RES>(P, A, (cudaStream_t)stream);
+  const int rc = run_elem<M_OBST_RES>(P, A, (cudaStream_t)stream);
+  P->last_wc = wcache;
+  return rc;
 }
 
 int hpgObstacleApplyD(hpgPlan P, const double* psi, const double* x, double* y, void* stream) {
@@ -439,7 +469,9 @@ int hpgGradientMoments(hpgPlan P, const double* psi, const double* phi, double* 
   if (!psi || !phi || !out) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
   A.in0 = psi; A.phi = phi; A.out = out; A.wc_out = wcache; A.flag = P->dflag;
-  return run_elem<M_GRAD_RES>(P, A, (cudaStream_t)stream);
+  const int rc = run_elem<M_GRAD_RES>(P, A, (cudaStream_t)stream);
+  P->last_wc = wcache;
+  return rc;
 }
 
 int hpgGradientApplyD(hpgPlan P, const double* psi, const double* phi, const double* x, double* y, void* stream) {
@@ -454,12 +486,127 @@ int hpgGradientApplyD(hpgPlan P, const double* psi, const double* phi, const dou
 
 int hpgApplyCached(hpgPlan P, const double* wcache, const double* x, double* y, void* stream) {
   HPG_NVTX("hpgApplyCached");
+  const double* prev_wc = P ? P->last_wc : nullptr;
   if (int rc = check(P)) return rc;
   if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   ElemArgs A = base_args(P);
   A.wc_in = wcache; A.in1 = x; A.out = y;
+  static const bool early_ok = getenv("HPG_NO_EARLY_WC") == nullptr;
+  A.wc_early = early_ok && prev_wc != wcache;
   if (P->kind == HPG_OBSTACLE) return run_elem<M_OBST_CACHED>(P, A, (cudaStream_t)stream);
   return run_elem<M_GRAD_CACHED>(P, A, (cudaStream_t)stream);
+}
+
+// U side of the residual: b_psi <- phi_mom - B^T u (obstacle) | -B^T u
+// (gradient); b_u on the dofs a cell owns alone, hat contributions to the edge
+// scratch (finished by k_hat_gather)
+static int uside_impl(hpgPlan P, const ElemArgs& A, cudaStream_t s) {
+  // thread-per-cell U side only when there are enough cells to fill the GPU;
+  // few cells (configs 0, 2, 3) go to the thread-per-entry kernel below
+  const bool many = P->N >= 8 * P->nsm;
+  if (many && usmall_available(P->p, P->kind == HPG_GRADIENT)) {
+    // low degree: thread per cell, generated straight-line code
+    return run_usmall(P->p, P->kind == HPG_GRADIENT, A, s);
+  }
+  if (many && P->kind == HPG_OBSTACLE && upass_available(P->p) && getenv("HPG_UPASS_OFF") == nullptr) {
+    // mid degree: warp per cell, generated separable passes
+    return run_upass(P->p, P->kind == HPG_GRADIENT, A, s);
+  }
+  // thread per cell-local entry
+  int TG = P->m * P->m;
+  TG = TG > 1024 ? 1024 : ((TG + 31) / 32) * 32;
+  // many mid-size cells (config 2): two entries per thread, so >= 2 CTAs
+  // fit an SM (register-limited) and all cells run in one wave
+  if (P->N >= P->nsm && TG > 512) TG = ((P->m * P->m + 1) / 2 + 31) / 32 * 32;
+  int cpb = 256 / TG;
+  if (cpb < 1) cpb = 1;
+  size_t smem = sizeof(double) * ((size_t)cpb * ((size_t)P->m * (P->m | 1) + 2 * (size_t)P->n * P->n) +
+                                  2 * P->m + 8);
+  if (smem > ((size_t)227 << 10)) return fail(HPG_ERR_UNSUPPORTED, "U tile too large for shared memory");
+  void* fn = P->kind == HPG_GRADIENT ? (void*)k_uside_pt<true> : (void*)k_uside_pt<false>;
+  if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // few large cells: split each cell's entries over several CTAs (one wave)
+  int usplit = 1;
+  if (cpb == 1 && P->N < P->nsm) {
+    const int blocks = (P->m * P->m + TG - 1) / TG;
+    usplit = P->nsm / P->N;
+    if (usplit > blocks) usplit = blocks;
+    if (usplit < 1) usplit = 1;
+  }
+  const dim3 grid((P->N + cpb - 1) / cpb * usplit), block(cpb * TG);
+  if (P->kind == HPG_GRADIENT)
+    CUDA_TRY(launch_pdl(k_uside_pt<true>, grid, block, smem, s, A, cpb, TG, usplit));
+  else
+    CUDA_TRY(launch_pdl(k_uside_pt<false>, grid, block, smem, s, A, cpb, TG, usplit));
+  CUDA_TRY(cudaGetLastError());
+  return HPG_OK;
+}
+
+static long long hat_count(const hpgPlan_st* P) {
+  return (long long)(P->ncx - 1) * P->niy + (long long)(P->nix - (P->ncx - 1)) * (P->ncy - 1);
+}
+
+static int hat_gather(hpgPlan P, const ElemArgs& A, cudaStream_t s) {
+  const long long nh = hat_count(P);
+  if (nh <= 0) return HPG_OK;
+  CUDA_TRY(launch_pdl(k_hat_gather, dim3((unsigned)((nh + 255) / 256)), dim3(256), 0, s, A));
+  CUDA_TRY(cudaGetLastError());
+  return HPG_OK;
+}
+
+// Few-cell plans (configs 0, 2, 3): the U side (+ hat gather) and, for
+// hpgResidualApply on the row-split path, the Jacobian apply from psi run on
+// the plan's two auxiliary streams concurrently with the psi-side quadrature,
+// which writes the plain moments M to a scratch vector; after the join one
+// elementwise kernel finishes b_psi = (phi_mom - B^T u) - M (obstacle) /
+// (-B^T u) + M (gradient) -- the same operations in the same order as the
+// sequential path, so the results are bitwise identical.  On the CTA path the
+// apply follows the join from the psi side's weight cache instead.
+static int residual_concurrent(hpgPlan P, ElemArgs A, double* wcache, const double* psi, const double* phi,
+                               const double* x, double* y, cudaStream_t s) {
+  const bool apply_aux = x != nullptr && P->path[P->kind == HPG_OBSTACLE ? M_OBST_APPLY : M_GRAD_APPLY] == PATH_WSPLIT;
+  double* wc = wcache;
+  if (x != nullptr && !apply_aux && wc == nullptr) wc = P->wscr;       // cached apply after the join
+  CUDA_TRY(cudaEventRecord(P->ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(P->aux[0], P->ev_fork, 0));
+  int rc;
+  // (a) U side + hat gather, concurrent
+  ElemArgs U = A;
+  U.residual = 1;
+  if ((rc = uside_impl(P, U, P->aux[0]))) return rc;
+  if ((rc = hat_gather(P, U, P->aux[0]))) return rc;
+  CUDA_TRY(cudaEventRecord(P->ev_join[0], P->aux[0]));
+  // (b) the Jacobian apply from psi, concurrent
+  if (apply_aux) {
+    CUDA_TRY(cudaStreamWaitEvent(P->aux[1], P->ev_fork, 0));
+    ElemArgs Ap = base_args(P);
+    Ap.in0 = psi; Ap.in1 = x; Ap.out = y;
+    if (P->kind == HPG_OBSTACLE) rc = run_elem<M_OBST_APPLY>(P, Ap, P->aux[1]);
+    else { Ap.phi = phi; rc = run_elem<M_GRAD_APPLY>(P, Ap, P->aux[1]); }
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(P->ev_join[1], P->aux[1]));
+  }
+  // (c) psi side: plain moments into the scratch (+ weight cache, flag)
+  ElemArgs Q = A;
+  Q.residual = 0;
+  Q.out = P->mscr;
+  Q.wc_out = wc;
+  rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, Q, s) : run_elem<M_GRAD_RES>(P, Q, s);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamWaitEvent(s, P->ev_join[0], 0));
+  if (apply_aux) CUDA_TRY(cudaStreamWaitEvent(s, P->ev_join[1], 0));
+  // (d) b_psi = (phi_mom - B^T u) - M | (-B^T u) + M
+  const long long n = P->ndof_psi;
+  k_residual_combine<<<(unsigned)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8), 256, 0, s>>>(
+      A.out, P->mscr, n, P->kind == HPG_GRADIENT);
+  CUDA_TRY(cudaGetLastError());
+  if (x != nullptr && !apply_aux) {
+    ElemArgs C = base_args(P);
+    C.wc_in = wc; C.in1 = x; C.out = y;
+    rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_CACHED>(P, C, s) : run_elem<M_GRAD_CACHED>(P, C, s);
+    if (rc) return rc;
+  }
+  return HPG_OK;
 }
 
 static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const double* u,
@@ -488,47 +635,9 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     if (x != nullptr) { A.in1 = x; A.wc_out = y; }
     return run_lowp(P->p, P->nq, x != nullptr, A, P->stab, s);
   }
-  // thread-per-cell U side only when there are enough cells to fill the GPU;
-  // few cells (config 0: 16) go to the thread-per-entry kernel below
-  const bool many = P->N >= 8 * P->nsm;
-  if (many && usmall_available(P->p, P->kind == HPG_GRADIENT)) {
-    // (1) U side, low degree: thread per cell, generated straight-line code
-    if ((rc = run_usmall(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
-  } else if (many && P->kind == HPG_OBSTACLE && upass_available(P->p) && getenv("HPG_UPASS_OFF") == nullptr) {
-    // (1) U side, mid degree: warp per cell, generated separable passes
-    if ((rc = run_upass(P->p, P->kind == HPG_GRADIENT, A, s))) return rc;
-  } else {
-    // (1) U side (thread per cell-local entry): b_psi <- phi_mom - B^T u
-    //     (obstacle) | -B^T u (gradient); b_u on owned dofs + edge scratch
-    int TG = P->m * P->m;
-    TG = TG > 1024 ? 1024 : ((TG + 31) / 32) * 32;
-    // many mid-size cells (config 2): two entries per thread, so >= 2 CTAs
-    // fit an SM (register-limited) and all cells run in one wave
-    if (P->N >= P->nsm && TG > 512) TG = ((P->m * P->m + 1) / 2 + 31) / 32 * 32;
-    int cpb = 256 / TG;
-    if (cpb < 1) cpb = 1;
-    size_t smem = sizeof(double) * ((size_t)cpb * ((size_t)P->m * (P->m | 1) + 2 * (size_t)P->n * P->n) +
-                                    2 * P->m + 8);
-    if (smem > ((size_t)227 << 10)) return fail(HPG_ERR_UNSUPPORTED, "U tile too large for shared memory");
-    void* fn = P->kind == HPG_GRADIENT ? (void*)k_uside_pt<true> : (void*)k_uside_pt<false>;
-    if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ElemArgs U = A;
-    // few large cells: split each cell's entries over several CTAs (one wave)
-    int usplit = 1;
-    if (cpb == 1 && P->N < P->nsm) {
-      const int blocks = (P->m * P->m + TG - 1) / TG;
-      usplit = P->nsm / P->N;
-      if (usplit > blocks) usplit = blocks;
-      if (usplit < 1) usplit = 1;
-    }
-    if (P->kind == HPG_GRADIENT)
-      CUDA_TRY(launch_pdl(k_uside_pt<true>, dim3((P->N + cpb - 1) / cpb * usplit), dim3(cpb * TG), smem, s, U, cpb,
-                          TG, usplit));
-    else
-      CUDA_TRY(launch_pdl(k_uside_pt<false>, dim3((P->N + cpb - 1) / cpb * usplit), dim3(cpb * TG), smem, s, U, cpb,
-                          TG, usplit));
-    CUDA_TRY(cudaGetLastError());
-  }
+  if (P->concurrent && !(P->small && wcache == nullptr)) return residual_concurrent(P, A, wcache, psi, phi, x, y, s);
+  // (1) U side
+  if ((rc = uside_impl(P, A, s))) return rc;
   // (2) psi side finishes b_psi in place (proximal.py:123 order)
   A.residual = 2;
   A.usmem = 0;
@@ -539,21 +648,14 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     if (x != nullptr) { A.in1 = x; A.wc_out = y; }
     rc = run_small(P->n, P->nq, true, x != nullptr, A, P->stab, s);
     x = nullptr;
-  } else if (x != nullptr && P->fused_ra) {
-    // few mid-size cells: residual + Jacobian apply in one row-split launch,
-    // D(psi)'s point weights handed over in shared memory (hpg_wsplit.cuh)
-    A.in1 = x;
-    A.wc_out = y;
-    rc = run_wsplit_ra(P->kind == HPG_GRADIENT, A, s);
-    x = nullptr;
   } else {
     rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, A, s) : run_elem<M_GRAD_RES>(P, A, s);
   }
   if (rc) return rc;
-  long long nh = (long long)(P->ncx - 1) * P->niy + (long long)(P->nix - (P->ncx - 1)) * (P->ncy - 1);
-  if (nh > 0) {
-    CUDA_TRY(launch_pdl(k_hat_gather, dim3((unsigned)((nh + 255) / 256)), dim3(256), 0, s, A));
-    CUDA_TRY(cudaGetLastError());
+  if (hat_count(P) > 0) {
+    if ((rc = hat_gather(P, A, s))) return rc;
+  } else {
+    P->last_wc = wcache;     // the psi-side kernel (the cache writer) was the last one
   }
   if (x != nullptr) {
     // Jacobian apply at the same psi (not fused on this path)
@@ -973,12 +1075,14 @@ int hpgStiffnessSolve(hpgPlan P, const double* b, double* x, void* stream) {
 int hpgSchurApply(hpgPlan P, const double* wcache, double alpha, double beta, const double* x, double* y,
                   void* stream) {
   HPG_NVTX("hpgSchurApply");
+  const double* prev_wc = P ? P->last_wc : nullptr;
   if (int rc = check(P)) return rc;
   if (!P->fdm_ready) return fail(HPG_ERR_ARG, "hpgStiffnessFactor has not been called on this plan");
   if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
   if (x == y) return fail(HPG_ERR_ARG, "in-place Schur apply is not supported");
   cudaStream_t s = (cudaStream_t)stream;
   int rc;
+  P->last_wc = prev_wc;          // the cached apply is this call's first kernel
   if ((rc = hpgApplyCached(P, wcache, x, P->syD, stream))) return rc;   // D x
   if ((rc = hpgBPsi(P, x, P->su1, stream))) return rc;                  // B x
   if ((rc = stiffness_solve(P, P->su1, P->su2, s))) return rc;          // A^{-1} B x

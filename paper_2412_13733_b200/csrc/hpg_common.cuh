@@ -100,6 +100,9 @@ struct ElemArgs {
   double* edge;      // [N][4m-4] hat-involved local contributions
   int usmem;         // doubles of U-side shared memory per thread group
   double* ubuf;      // CTA path, large m: U-side buffers in global scratch [N][usmem]
+  int wc_early;      // cached apply: the weight cache was not written by the
+                     // immediately preceding kernel, so it may be prefetched
+                     // before griddepcontrol.wait (hpgApplyCached decides)
 };
 
 struct WarpSync { __device__ __forceinline__ void operator()() const { __syncwarp(); } };

@@ -245,10 +245,12 @@ k_warp(ElemArgs A) {
   }
   cp_async_commit();
   for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
-  // only the (constant) tables are copied before the grid-dependency wait:
-  // PDL makes the previous grid's writes visible after griddepcontrol.wait
-  // and not before, so the weight cache -- which the immediately preceding
-  // kernel may have written -- is read after it
+  // before the grid-dependency wait only the (constant) tables are copied --
+  // PDL makes the previous grid's writes visible after griddepcontrol.wait,
+  // not before -- and, when the host knows the weight cache was NOT written
+  // by the immediately preceding kernel (A.wc_early, set by hpgApplyCached
+  // from the plan's call history; cache writers never trigger their
+  // dependents early), the first cell's weights
   int buf = 0;
   // ROLL: one row tile's weights into half h of the warp's slice
   auto load_rt = [&](int e, int rt, int h) {
@@ -272,10 +274,12 @@ k_warp(ElemArgs A) {
   };
   const int stride = gridDim.x * W;
   int e = blockIdx.x * W + warp;
-  // one wave: let the next kernel in the stream start its (table) prologue now
-  pdl_trigger();
+  if (A.wc_early && e < A.N) load_weights(e, 0);
+  // one wave: let the next kernel in the stream start its prologue now --
+  // except a kernel writing a weight cache (see above)
+  if (!(CF::WRITES_WC && A.wc_out != nullptr)) pdl_trigger();
   pdl_wait();
-  if (e < A.N) load_weights(e, 0);
+  if (!A.wc_early && e < A.N) load_weights(e, 0);
 
   using XFrag = double[REGX ? NIN : 1][REGX ? NK : 1][REGX ? NT : 1];
   XFrag X, Xn;

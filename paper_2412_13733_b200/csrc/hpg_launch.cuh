@@ -51,11 +51,6 @@ template <int MODE> bool wsplit_available(int NT, int QT);
 // row-tile splits + a deterministic reduction).
 template <int MODE> int run_mode(int path, ElemArgs A, cudaStream_t s);
 
-// Fused residual + Jacobian apply, row-split (hpg_wsplit_ra.cu): A.out =
-// b_psi (residual combine), A.wc_out = y.
-bool wsplit_ra_available(bool gradient, int NT, int QT);
-int run_wsplit_ra(bool gradient, const ElemArgs& A, cudaStream_t s);
-
 // Thread-per-element low-degree obstacle kernel (hpg_small.cuh).
 struct SmallTables;
 bool small_available(int n, int q);

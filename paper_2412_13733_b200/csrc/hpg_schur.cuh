@@ -18,6 +18,14 @@
 
 namespace hpg {
 
+// b_psi = (phi_mom - B^T u) - M (obstacle) | (-B^T u) + M (gradient): the
+// residual's last step when the U side ran concurrently (residual_concurrent)
+__global__ void k_residual_combine(double* __restrict__ bpsi, const double* __restrict__ m, long long n,
+                                   bool gradient) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    bpsi[i] = gradient ? bpsi[i] + m[i] : bpsi[i] - m[i];
+}
+
 // y = -((yD + E x) + z / alpha) over the global psi vector
 __global__ void k_schur_combine(ElemArgs A, int gradient, double alpha, double beta, const double* __restrict__ x,
                                 const double* __restrict__ yD, const double* __restrict__ z,

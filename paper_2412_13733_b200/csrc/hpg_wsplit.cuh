@@ -12,14 +12,7 @@
 // CellKernel2D.moments, assembly.py:249-251; residual modes finish b_psi in
 // place, proximal.py:123,125).
 //
-// k_wsplit<NT,QT,MODE>: one mode, QT warps.
-// k_wsplit_ra<NT,QT,MR,MC>: the residual AND the Jacobian apply at the same
-// psi (hpgResidualApply: the k_mv = 1 step of configs 0 and 2) in one launch
-// of 2 QT warps: warp rt of the first group runs the residual mode MR and
-// hands its row tile's point weights of D(psi) to warp rt of the second group
-// through shared memory (a named barrier per row tile); that warp applies them
-// to the direction x (cached mode MC).  The weights never touch HBM and the
-// apply's x synthesis overlaps the residual's.
+// k_wsplit<NT,QT,MODE>: one mode, QT warps (ws_rowtile is the per-warp body).
 #pragma once
 #include "hpg_elem.cuh"
 
@@ -39,13 +32,6 @@ struct WsplitCfg {
   static constexpr int BODY = (TILES + WTS) > YPART ? (TILES + WTS) : YPART;
   static constexpr int SMEM_DBL = TAB + INV + BODY;
 };
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // One warp, one row tile rt of element e: accumulates MODE's Y partial into
 // Y.  sTile: this mode's coefficient tiles (fields in field_src order).
@@ -254,7 +240,8 @@ k_wsplit(ElemArgs A) {
   }
   cp_async_commit();
   for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
-  pdl_trigger();
+  // a kernel writing a weight cache never releases its dependents early
+  if (!((MODE == M_OBST_RES || MODE == M_GRAD_RES) && A.wc_out != nullptr)) pdl_trigger();
   pdl_wait();
   if (e >= A.N) return;
   const int cx = e / A.ncy, cy = e - cx * A.ncy;
@@ -280,87 +267,6 @@ k_wsplit(ElemArgs A) {
   ws_store_partial<NT, NOUT>(Y, sY + (size_t)rt * NOUT * NP * NP);
   __syncthreads();
   ws_reduce_write<NT, QT, MODE>(A, e, sY, sInv, threadIdx.x, blockDim.x);
-}
-
-// residual (MR) + Jacobian apply (MC) at the same psi, weights through smem
-template <int NT, int QT, int MR, int MC>
-struct WsplitRaCfg {
-  using CR = WsplitCfg<NT, QT, MR>;
-  using TRR = ModeTraits<MR>;
-  using TRC = ModeTraits<MC>;
-  static constexpr int NP = CR::NP, QP = CR::QP, TILE = CR::TILE;
-  static constexpr int NINR = TRR::NIN, NINC = TRC::NIN, NOUT = TRR::NOUT;
-  static constexpr int WROW = QT * TRR::NW * 64;
-  static constexpr int TILES = (NINR + NINC) * TILE;
-  static constexpr int WTS = QT * WROW;
-  static constexpr int YPART = 2 * QT * NOUT * NP * NP;
-  static constexpr int BODY = (TILES + WTS) > YPART ? (TILES + WTS) : YPART;
-  static constexpr int SMEM_DBL = CR::TAB + CR::INV + BODY;
-};
-
-template <int NT, int QT, int MR, int MC>
-__global__ void __launch_bounds__(64 * QT, 1)
-k_wsplit_ra(ElemArgs A) {
-  using CF = WsplitRaCfg<NT, QT, MR, MC>;
-  constexpr int NP = CF::NP, QP = CF::QP, NOUT = CF::NOUT, TILE = CF::TILE;
-  static_assert(ModeTraits<MR>::NOUT == ModeTraits<MC>::NOUT, "residual and apply output counts");
-  extern __shared__ double smem[];
-  double* sS = smem;
-  double* sT = sS + QP * NP;
-  double* sInv = sT + NP * QP;
-  double* sBody = sInv + WsplitCfg<NT, QT, MR>::INV;
-  double* sTileR = sBody;                          // psi fields
-  double* sTileC = sBody + CF::NINR * TILE;        // x fields
-  double* sW = sBody + CF::TILES;                  // [rt][ht][w][lane][2]
-  double* sY = sBody;                              // [group][rt][NOUT][NP][NP] at the end
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = warp / QT, rt = warp - grp * QT, e = blockIdx.x;
-  for (int i = 2 * threadIdx.x; i < QP * NP; i += 2 * blockDim.x) {
-    cp_async16(sS + i, A.Sf + i);
-    cp_async16(sT + i, A.Tf + i);
-  }
-  cp_async_commit();
-  for (int i = threadIdx.x; i < NP; i += blockDim.x) sInv[i] = kInvOdd[i];
-  pdl_trigger();
-  pdl_wait();
-  if (e >= A.N) return;
-  const int cx = e / A.ncy, cy = e - cx * A.ncy;
-  ws_stage_tiles<NP, MR>(A, cx, cy, 0, CF::NINR, sTileR);
-  ws_stage_tiles<NP, MC>(A, cx, cy, 0, CF::NINC, sTileC);
-  cp_async_wait_all();
-  __syncthreads();
-  double Y[NOUT][NT][NT][2];
-  bool flag = false;
-  double* wrow = sW + rt * CF::WROW;
-  const int bar = 1 + rt;                          // named barrier of row tile rt (ids 1..QT)
-  if (grp == 0) {
-    // residual: the apply's weights of this row tile leave through wrow
-    ElemArgs R = A;
-    R.wc_out = nullptr;
-    ws_rowtile<NT, QT, MR>(R, e, rt, sS, sT, sTileR, nullptr, wrow, Y, flag, [] {}, [&] {
-      __threadfence_block();
-      named_bar_arrive(bar, 64);
-    });
-  } else {
-    ws_rowtile<NT, QT, MC>(A, e, rt, sS, sT, sTileC, wrow, nullptr, Y, flag,
-                           [&] { named_bar_sync(bar, 64); }, [] {});
-  }
-  if constexpr (MR == M_OBST_RES) {
-    if (grp == 0 && __any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
-  }
-  __syncthreads();          // tiles and weights are dead: the body holds the partials
-  ws_store_partial<NT, NOUT>(Y, sY + ((size_t)grp * QT + rt) * NOUT * NP * NP);
-  __syncthreads();
-  const int half = 32 * QT;
-  if (threadIdx.x < half) {
-    ws_reduce_write<NT, QT, MR>(A, e, sY, sInv, threadIdx.x, half);
-  } else {
-    // the apply's moments go to y (A.wc_out on this path), plain (no residual combine)
-    ElemArgs B = A;
-    B.out = A.wc_out;
-    B.residual = 0;
-    ws_reduce_write<NT, QT, MC>(B, e, sY + (size_t)QT * NOUT * NP * NP, sInv, threadIdx.x - half, half);
-  }
 }
 
 }  // namespace hpg
