@@ -6,6 +6,7 @@
 #include "hpg_elem.cuh"
 #include "hpg_launch.cuh"
 #include "hpg_wsplit.cuh"
+#include "hpg_big.cuh"
 
 #ifndef HPG_WSPLIT_LIST
 #define HPG_WSPLIT_LIST
@@ -181,6 +182,72 @@ int launch_cta_t(ElemArgs A, cudaStream_t s) {
   return 0;
 }
 
+// config 3 (Gauss): the on-chip large-tile kernel (hpg_big.cuh), same split
+// reduction as k_cta
+template <int MODE, int NT, int QT, int RB, int W>
+int launch_big_t(ElemArgs A, cudaStream_t s) {
+  using CF = BigCfg<MODE, NT, QT, RB, W>;
+  const size_t smem = sizeof(double) * (size_t)CF::SMEM_DBL;
+  struct Memo { size_t attr = 0; int ok_n = -1, ok_res = 0; };
+  static PerDevice<Memo> memo;
+  A.cluster_red = 0;
+  const bool try_cluster = A.splits > 1 && A.splits <= 8 && getenv("HPG_NO_CLUSTER") == nullptr;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if (smem > m.attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_big<MODE, NT, QT, RB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      m.attr = smem;
+    }
+    if (try_cluster && m.ok_n != A.N) {
+      m.ok_n = A.N;
+      m.ok_res = 0;
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(A.N * A.splits);
+      q.blockDim = dim3(32 * W);
+      q.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = A.splits; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int nclusters = 0;
+      cudaError_t qe = cudaOccupancyMaxActiveClusters(&nclusters, k_big<MODE, NT, QT, RB, W>, &q);
+      if (qe == cudaSuccess && nclusters >= A.N) m.ok_res = 1;
+      cudaGetLastError();
+    }
+    A.cluster_red = try_cluster ? m.ok_res : 0;
+    return cudaSuccess;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_big)", se);
+  cudaError_t e;
+  if (A.cluster_red) {
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(A.N * A.splits);
+    q.blockDim = dim3(32 * W);
+    q.dynamicSmemBytes = smem;
+    q.stream = s;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = A.splits; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    e = cudaLaunchKernelEx(&q, k_big<MODE, NT, QT, RB, W>, A);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_big cluster launch", e);
+  }
+  e = launch_pdl(k_big<MODE, NT, QT, RB, W>, dim3(A.N * A.splits), dim3(32 * W), smem, s, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_big launch", e);
+  if (A.splits > 1) {
+    const long long total = (long long)A.N * ModeTraits<MODE>::NOUT * A.n * A.n;
+    e = launch_pdl(k_cta_reduce<MODE>, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, A);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "k_cta_reduce launch", e);
+  }
+  return 0;
+}
+
 // few elements split across CTAs (config 3): 16 warps per CTA for latency
 // hiding; many elements (config 2): 8 warps per CTA, more CTAs per SM
 template <int MODE, int W>
@@ -195,6 +262,10 @@ int launch_cta_w(ElemArgs A, cudaStream_t s) {
 
 template <int MODE>
 int launch_cta(ElemArgs A, cudaStream_t s) {
+  if constexpr (MODE == M_OBST_RES || MODE == M_OBST_APPLY || MODE == M_OBST_CACHED) {
+    if (A.NT == 11 && A.QT == 16 && A.splits == 8 && getenv("HPG_NO_BIG") == nullptr)
+      return launch_big_t<MODE, 11, 16, 2, 16>(A, s);
+  }
   if (A.splits > 1) return launch_cta_w<MODE, 16>(A, s);
   return launch_cta_w<MODE, 8>(A, s);
 }
