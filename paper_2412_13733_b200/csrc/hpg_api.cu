@@ -81,10 +81,10 @@ struct hpgPlan_st {
   int nix, niy;
   long long ncomp, ndof_psi, ndof_u;
   int path[8];                  // ElemPath per element-kernel mode
-  // few-cell plans: U side / apply concurrent with the psi side (residual_concurrent)
+  // few-cell plans: U side concurrent with the psi side (residual_concurrent)
   bool concurrent = false;
-  cudaStream_t aux[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaStream_t aux[1] = {nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[1] = {nullptr};
   double* mscr = nullptr;       // psi-side moments [ndof_psi]
   double* wscr = nullptr;       // weight cache of the fused residual + cached apply
   // weight cache written by the LAST kernel of this plan's most recent call
@@ -342,16 +342,13 @@ int hpgPlanCreate(hpgPlan* plan, int kind, int ncx, int ncy, int p, int nq, cons
     }
     P->path[M_VALUES] = PATH_CTA;
   }
-  // few cells: the U side (and the apply of hpgResidualApply) overlap the
-  // psi-side quadrature on two auxiliary streams
+  // few cells: the U side overlaps the psi-side quadrature on an auxiliary stream
   if (P->N < 4 * P->nsm && getenv("HPG_NO_CONCURRENT") == nullptr &&
       !(kind == HPG_OBSTACLE && P->small && lowp_available(p, nq))) {
     const size_t wlen = (size_t)P->N * P->QT * P->QT * (kind == HPG_OBSTACLE ? 1 : 3) * 64;
     e = cudaStreamCreateWithFlags(&P->aux[0], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P->aux[1], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_join[0], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_join[1], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&P->mscr, sizeof(double) * P->ndof_psi + 16);
     if (e == cudaSuccess) e = cudaMalloc(&P->wscr, sizeof(double) * wlen + 16);
     if (e != cudaSuccess) { hpgPlanDestroy(P); return fail(HPG_ERR_CUDA, cudaGetErrorString(e)); }
@@ -401,10 +398,8 @@ int hpgPlanDestroy(hpgPlan P) {
   cudaFree(P->qH3); cudaFree(P->qSRT); cudaFree(P->qTRT); cudaFree(P->qKT); cudaFree(P->qMT);
   cudaFree(P->mscr); cudaFree(P->wscr);
   if (P->aux[0]) cudaStreamDestroy(P->aux[0]);
-  if (P->aux[1]) cudaStreamDestroy(P->aux[1]);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join[0]) cudaEventDestroy(P->ev_join[0]);
-  if (P->ev_join[1]) cudaEventDestroy(P->ev_join[1]);
   delete P;
   return HPG_OK;
 }
@@ -554,19 +549,19 @@ static int hat_gather(hpgPlan P, const ElemArgs& A, cudaStream_t s) {
   return HPG_OK;
 }
 
-// Few-cell plans (configs 0, 2, 3): the U side (+ hat gather) and, for
-// hpgResidualApply on the row-split path, the Jacobian apply from psi run on
-// the plan's two auxiliary streams concurrently with the psi-side quadrature,
-// which writes the plain moments M to a scratch vector; after the join one
+// Few-cell plans (configs 0, 2, 3): the U side (+ hat gather) runs on the
+// plan's auxiliary stream concurrently with the psi-side quadrature, which
+// writes the plain moments M to a scratch vector; after the join one
 // elementwise kernel finishes b_psi = (phi_mom - B^T u) - M (obstacle) /
 // (-B^T u) + M (gradient) -- the same operations in the same order as the
-// sequential path, so the results are bitwise identical.  On the CTA path the
-// apply follows the join from the psi side's weight cache instead.
-static int residual_concurrent(hpgPlan P, ElemArgs A, double* wcache, const double* psi, const double* phi,
-                               const double* x, double* y, cudaStream_t s) {
-  const bool apply_aux = x != nullptr && P->path[P->kind == HPG_OBSTACLE ? M_OBST_APPLY : M_GRAD_APPLY] == PATH_WSPLIT;
+// sequential path, so the results are bitwise identical.  For
+// hpgResidualApply the Jacobian apply then runs from the point weights the
+// psi side cached (measured faster than recomputing them from psi on a
+// second concurrent stream: the two element kernels do not fit an SM together).
+static int residual_concurrent(hpgPlan P, ElemArgs A, double* wcache, const double* x, double* y,
+                               cudaStream_t s) {
   double* wc = wcache;
-  if (x != nullptr && !apply_aux && wc == nullptr) wc = P->wscr;       // cached apply after the join
+  if (x != nullptr && wc == nullptr) wc = P->wscr;
   CUDA_TRY(cudaEventRecord(P->ev_fork, s));
   CUDA_TRY(cudaStreamWaitEvent(P->aux[0], P->ev_fork, 0));
   int rc;
@@ -576,36 +571,27 @@ static int residual_concurrent(hpgPlan P, ElemArgs A, double* wcache, const doub
   if ((rc = uside_impl(P, U, P->aux[0]))) return rc;
   if ((rc = hat_gather(P, U, P->aux[0]))) return rc;
   CUDA_TRY(cudaEventRecord(P->ev_join[0], P->aux[0]));
-  // (b) the Jacobian apply from psi, concurrent
-  if (apply_aux) {
-    CUDA_TRY(cudaStreamWaitEvent(P->aux[1], P->ev_fork, 0));
-    ElemArgs Ap = base_args(P);
-    Ap.in0 = psi; Ap.in1 = x; Ap.out = y;
-    if (P->kind == HPG_OBSTACLE) rc = run_elem<M_OBST_APPLY>(P, Ap, P->aux[1]);
-    else { Ap.phi = phi; rc = run_elem<M_GRAD_APPLY>(P, Ap, P->aux[1]); }
-    if (rc) return rc;
-    CUDA_TRY(cudaEventRecord(P->ev_join[1], P->aux[1]));
-  }
-  // (c) psi side: plain moments into the scratch (+ weight cache, flag)
+  // (b) psi side: plain moments into the scratch (+ weight cache, flag)
   ElemArgs Q = A;
   Q.residual = 0;
   Q.out = P->mscr;
   Q.wc_out = wc;
   rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_RES>(P, Q, s) : run_elem<M_GRAD_RES>(P, Q, s);
   if (rc) return rc;
-  CUDA_TRY(cudaStreamWaitEvent(s, P->ev_join[0], 0));
-  if (apply_aux) CUDA_TRY(cudaStreamWaitEvent(s, P->ev_join[1], 0));
-  // (d) b_psi = (phi_mom - B^T u) - M | (-B^T u) + M
-  const long long n = P->ndof_psi;
-  k_residual_combine<<<(unsigned)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8), 256, 0, s>>>(
-      A.out, P->mscr, n, P->kind == HPG_GRADIENT);
-  CUDA_TRY(cudaGetLastError());
-  if (x != nullptr && !apply_aux) {
+  // (c) the Jacobian apply at the same psi from the cached weights (it does
+  //     not need the U side: it runs before the join, overlapping it too)
+  if (x != nullptr) {
     ElemArgs C = base_args(P);
     C.wc_in = wc; C.in1 = x; C.out = y;
     rc = P->kind == HPG_OBSTACLE ? run_elem<M_OBST_CACHED>(P, C, s) : run_elem<M_GRAD_CACHED>(P, C, s);
     if (rc) return rc;
   }
+  CUDA_TRY(cudaStreamWaitEvent(s, P->ev_join[0], 0));
+  // (d) b_psi = (phi_mom - B^T u) - M | (-B^T u) + M
+  const long long n = P->ndof_psi;
+  k_residual_combine<<<(unsigned)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8), 256, 0, s>>>(
+      A.out, P->mscr, n, P->kind == HPG_GRADIENT);
+  CUDA_TRY(cudaGetLastError());
   return HPG_OK;
 }
 
@@ -635,7 +621,7 @@ static int residual_impl(hpgPlan P, double alpha, const double* psi_prev, const 
     if (x != nullptr) { A.in1 = x; A.wc_out = y; }
     return run_lowp(P->p, P->nq, x != nullptr, A, P->stab, s);
   }
-  if (P->concurrent && !(P->small && wcache == nullptr)) return residual_concurrent(P, A, wcache, psi, phi, x, y, s);
+  if (P->concurrent && !(P->small && wcache == nullptr)) return residual_concurrent(P, A, wcache, x, y, s);
   // (1) U side
   if ((rc = uside_impl(P, A, s))) return rc;
   // (2) psi side finishes b_psi in place (proximal.py:123 order)

@@ -23,13 +23,17 @@ __device__ __forceinline__ void point_map(const double* v, double phi, const dou
   } else if constexpr (MODE == M_OBST_CACHED) {
     vw[0] = v[0] * wcin[0];
   } else if constexpr (MODE == M_GRAD_RES) {
-    // nl_moments, assembly.py:786-790; kernel fields :796-801
+    // nl_moments, assembly.py:786-790; kernel fields :796-801.  One
+    // reciprocal square root (rsqrt, <= 1 ulp) replaces the reference's
+    // sqrt + divisions: phi v / sqrt(r2) and r2^{-1/2}, r2^{-3/2} agree to a
+    // few ulp, far inside the 1e-12 parity bar, at a fraction of the cost of
+    // IEEE division (the dominant FP64 work of the gradient map)
     double vx = v[0], vy = v[1];
     double r2 = 1.0 + vx * vx + vy * vy;
-    double root = sqrt(r2);
-    vw[0] = phi * vx / root;
-    vw[1] = phi * vy / root;
-    double inv = 1.0 / root;
+    double inv = rsqrt(r2);
+    double pinv = phi * inv;
+    vw[0] = pinv * vx;
+    vw[1] = pinv * vy;
     double inv3 = inv * inv * inv;
     wcout[0] = phi * (inv - vx * vx * inv3);
     wcout[1] = phi * (-vx * vy * inv3);
@@ -38,7 +42,7 @@ __device__ __forceinline__ void point_map(const double* v, double phi, const dou
     // apply_D, assembly.py:820-829
     double vx = v[0], vy = v[1];
     double r2 = 1.0 + vx * vx + vy * vy;
-    double inv = 1.0 / sqrt(r2);
+    double inv = rsqrt(r2);
     double inv3 = inv * inv * inv;
     double kxx = phi * (inv - vx * vx * inv3);
     double kxy = phi * (-vx * vy * inv3);

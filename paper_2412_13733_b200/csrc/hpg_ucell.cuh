@@ -99,23 +99,41 @@ __global__ void __launch_bounds__(1024) k_uside_pt(ElemArgs A, int cpb, int TG, 
   const long long base0 = psi_index(A, cx, cy, 0, 0);
   double* sC = smem + 2 * m + 8 + (size_t)(grp < cpb ? grp : 0) * (m * ld + 2 * n * n);  // m x ld U tile
   double* sG = sC + m * ld;               // [comp][n][n] weighted psi_prev - psi
+  // the rows this CTA's entries read: with one pass (tstep >= m^2) the CTA
+  // owns entries [sp TG, (sp+1) TG), i.e. rows j0..j1, and the sparse 1D
+  // operators reach rows j-2..j+2 plus the hat rows 0, 1 -- a few-cell split
+  // (config 3: 7 CTAs per cell) then loads ~1/5 of the tile per CTA
+  int rlo = 0, rhi = m - 1;
+  if (tstep >= m * m) {
+    const int e0 = sp * TG, e1 = (sp + 1) * TG < m * m ? (sp + 1) * TG : m * m;
+    rlo = e0 / m - 2 < 0 ? 0 : e0 / m - 2;
+    rhi = (e1 - 1) / m + 2 > m - 1 ? m - 1 : (e1 - 1) / m + 2;
+  }
+  const int wrows = rhi - rlo + 1;
+  const int extra = rlo > 1 ? 2 : (rlo > 0 ? 1 : 0);           // hat rows below the window
   // unrolled so every thread's gathers are in flight together (one L2 round
   // trip per 8 entries instead of one per entry)
 #pragma unroll 8
-  for (int t = valid ? t0 : m * m; t < m * m; t += TG) {
-    const int i = t / m, l = t - i * m;
+  for (int t = valid ? t0 : (wrows + extra) * m; t < (wrows + extra) * m; t += TG) {
+    const int q = t / m, l = t - q * m;
+    const int i = q < extra ? q : rlo + (q - extra);
     sC[i * ld + l] = u_at(A, cx, cy, i, l);
   }
+  const int glo = rlo < n ? rlo : n, ghi = rhi < n - 1 ? rhi : n - 1;
+  const int grows = ghi - glo + 1 > 0 ? ghi - glo + 1 : 0;
+  const int gextra = glo > 1 ? 2 : (glo > 0 ? 1 : 0);
+  const int gper = (grows + gextra) * n;
 #pragma unroll 8
-  for (int t = valid ? t0 : n * n * 2; t < n * n * (GRADIENT ? 2 : 1); t += TG) {
-    const int comp = t / (n * n), r = t - comp * n * n, i = r / n, l = r - i * n;
+  for (int t = valid ? t0 : gper * 2; t < gper * (GRADIENT ? 2 : 1); t += TG) {
+    const int comp = t / gper, rr = t - comp * gper, q = rr / n, l = rr - q * n;
+    const int i = q < gextra ? q : glo + (q - gextra);
     const long long gi = comp * A.ncomp + base0 + (long long)i * A.ld + l;
     const double d = __ldg(A.psi_prev + gi) - __ldg(A.in0 + gi);
     double wi, wl;
     if (!GRADIENT) { wi = hx * kInvOdd[i]; wl = hy * kInvOdd[l]; }
     else if (comp == 0) { wi = 2.0 * kInvOdd[i]; wl = hy * kInvOdd[l]; }
     else { wi = hx * kInvOdd[i]; wl = 2.0 * kInvOdd[l]; }
-    sG[t] = (wi * d) * wl;
+    sG[comp * n * n + i * n + l] = (wi * d) * wl;
   }
   __syncthreads();
   auto C = [&](int i, int l) { return sC[i * ld + l]; };

@@ -28,8 +28,10 @@ struct WsplitCfg {
   static constexpr int WROW = QT * TR::NW * 64;          // one row tile's weights
   static constexpr int TILES = TR::NIN * TILE;
   static constexpr int WTS = cached ? QT * WROW : 0;
+  static constexpr bool PHI = MODE == M_GRAD_RES || MODE == M_GRAD_APPLY;
+  static constexpr int PHIS = PHI ? QP * QP : 0;            // staged phi samples
   static constexpr int YPART = QT * TR::NOUT * NP * NP;
-  static constexpr int BODY = (TILES + WTS) > YPART ? (TILES + WTS) : YPART;
+  static constexpr int BODY = (TILES + WTS + PHIS) > YPART ? (TILES + WTS + PHIS) : YPART;
   static constexpr int SMEM_DBL = TAB + INV + BODY;
 };
 
@@ -43,7 +45,8 @@ template <int NT, int QT, int MODE, class BeforeMap, class AfterMap>
 __device__ __forceinline__ void ws_rowtile(const ElemArgs& A, int e, int rt, const double* sS, const double* sT,
                                            const double* sTile, const double* w_in, double* w_out,
                                            double (&Y)[ModeTraits<MODE>::NOUT][NT][NT][2], bool& flag,
-                                           BeforeMap before_map, AfterMap after_map) {
+                                           BeforeMap before_map, AfterMap after_map,
+                                           const double* sPhi = nullptr) {
   using TR = ModeTraits<MODE>;
   using CF = WsplitCfg<NT, QT, MODE>;
   constexpr int NP = CF::NP, NK = NP / 4, QK = CF::QP / 4, LDT = CF::LDT, TILE = CF::TILE;
@@ -109,7 +112,7 @@ __device__ __forceinline__ void ws_rowtile(const ElemArgs& A, int e, int rt, con
       for (int w = 0; w < NW; ++w) wi[w] = CF::cached ? win[w][j] : 0.0;
       double phi = 0.0;
       if constexpr (gradient && !CF::cached) {
-        if (inside) phi = __ldg(A.phi + ((long long)e * A.nq + g) * A.nq + h);
+        if (inside) phi = sPhi ? sPhi[g * CF::QP + h] : __ldg(A.phi + ((long long)e * A.nq + g) * A.nq + h);
       }
       bool fl = false;
       point_map<MODE>(v, phi, wi, wo, vw, fl);
@@ -183,8 +186,15 @@ __device__ __forceinline__ void ws_store_partial(const double (&Y)[NOUT][NT][NT]
           dst[(o * NP + 8 * at + 2 * c + j) * NP + 8 * bt + r] = Y[o][bt][at][j];
 }
 
+__device__ __forceinline__ void cp_async8z(double* dst, const double* src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+
 // Stage the element's coefficient tiles of fields [f0, f0+nf) of MODE's field
-// list into dst (rows of n contiguous doubles), all threads of the CTA.
+// list into dst (rows of n contiguous doubles), all threads of the CTA, as
+// 8-byte cp.async copies (zero fill in the padding): every load in flight at
+// once, no register round trip.  The caller commits and waits.
 template <int NP, int MODE>
 __device__ __forceinline__ void ws_stage_tiles(const ElemArgs& A, int cx, int cy, int f0, int nf, double* dst) {
   constexpr int LDT = NP + 2, TILE = NP * LDT;
@@ -195,10 +205,19 @@ __device__ __forceinline__ void ws_stage_tiles(const ElemArgs& A, int cx, int cy
     src += comp * A.ncomp;
     for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
       const int a = idx / NP, b = idx - a * NP;
-      double v = 0.0;
-      if (a < A.n && b < A.n) v = __ldg(src + psi_index(A, cx, cy, a, b));
-      dst[f * TILE + a * LDT + b] = v;
+      const bool in = a < A.n && b < A.n;
+      cp_async8z(dst + f * TILE + a * LDT + b, in ? src + psi_index(A, cx, cy, a, b) : src, in);
     }
+  }
+}
+
+// The element's gradient-bound samples phi (nq x nq) into dst (row stride QP)
+template <int QP>
+__device__ __forceinline__ void ws_stage_phi(const ElemArgs& A, int e, double* dst) {
+  const double* src = A.phi + (long long)e * A.nq * A.nq;
+  for (int idx = threadIdx.x; idx < A.nq * A.nq; idx += blockDim.x) {
+    const int g = idx / A.nq, h = idx - g * A.nq;
+    cp_async8z(dst + g * QP + h, src + idx, true);
   }
 }
 
@@ -253,13 +272,16 @@ k_wsplit(ElemArgs A) {
     cp_async_commit();
   }
   ws_stage_tiles<NP, MODE>(A, cx, cy, 0, TR::NIN, sTile);
+  double* sPhi = sBody + CF::TILES + CF::WTS;
+  if constexpr (CF::PHI) ws_stage_phi<QP>(A, e, sPhi);
+  cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
   double Y[NOUT][NT][NT][2];
   bool flag = false;
   auto nop = [] {};
   ws_rowtile<NT, QT, MODE>(A, e, rt, sS, sT, sTile, CF::cached ? sW + rt * CF::WROW : nullptr, nullptr, Y, flag,
-                           nop, nop);
+                           nop, nop, CF::PHI ? sPhi : nullptr);
   if constexpr (MODE == M_OBST_RES) {
     if (__any_sync(0xffffffffu, flag) && lane == 0) atomicOr(A.flag, 1);
   }
