@@ -126,6 +126,19 @@ __global__ void __launch_bounds__(LOWP_TH, P <= 4 ? HPG_LOWP_MINB_SMALL : 1) k_l
       if (APPLY) MY[a][b] = 0.0;
     }
   bool flag = false;
+  if constexpr (N == 1) {
+    // p = 2: the psi tile is ONE Legendre coefficient and P_0 = 1 at every
+    // point, so the synthesized field is that coefficient everywhere: one
+    // clamped exp per cell instead of Q^2, and M = E (sum_g T_0g)^2 (the
+    // reference's T E T^T regrouped; equal to rounding)
+    double sT = 0.0;
+#pragma unroll
+    for (int h = 0; h < Q; ++h) sT += tb.T[h];
+    const double v = tb.S[0] * sC[0][0][tid];        // S[g][0] = P_0 = 1
+    const double E = clamped_exp_neg(v, flag);
+    Mm[0][0] = (E * sT) * sT;
+    if (APPLY) MY[0][0] = ((E * (tb.S[0] * sC[NIN - 1][0][tid])) * sT) * sT;
+  } else {
 #pragma unroll 1
   for (int g = 0; g < Q; ++g) {
     double Pv[N], PX[APPLY ? N : 1];
@@ -171,6 +184,7 @@ __global__ void __launch_bounds__(LOWP_TH, P <= 4 ? HPG_LOWP_MINB_SMALL : 1) k_l
         if (APPLY) MY[a][b] = fma(t, exv[b], MY[a][b]);
       }
     }
+  }
   }
   if (flag) atomicOr(A.flag, 1);
   const double hx = A.hx[cx], hy = A.hy[cy];
