@@ -275,3 +275,28 @@ def test_qvi_phi_moments_assignment_reaches_device():
     assert rel_err(r_dev[1], r_ref[1]) < 1e-12
     assert rel_err(r_dev[0], r_ref[0]) < 1e-12
     del torch
+
+
+def test_reference_solve_with_device_preconditioner(monkeypatch):
+    """INTEGRATION.md §2's one-line adoption: the reference's
+    schur_preconditioner (linalg.py:262-264) returning the device per-cell LU;
+    the rest of proximal.solve unmodified."""
+    from hpgalerkin import linalg, proximal
+    from paper_2412_13733_b200.workloads import phi_sin
+    orig = linalg.schur_preconditioner
+
+    def device_preconditioner(disc, D, alpha, beta):
+        if hasattr(disc, "device_disc"):
+            return disc.device_disc.schur_preconditioner(D.device_matrix, alpha, beta)
+        return orig(disc, D, alpha, beta)
+
+    monkeypatch.setattr(linalg, "schur_preconditioner", device_preconditioner)
+    for name in ("obst_p6_gauss", "obst_p8_ref"):
+        g = load_solve(name)
+        disc = _b200_disc("obstacle", _mesh(g["xpts"], g["ypts"], g["p"]), 1.0, phi_sin, g["rule"], g["nq"])
+        sched = proximal.AlphaSchedule(alpha0=g["alpha0"], rate=2.0, alpha_max=g["alpha_max"])
+        rep = proximal.solve(disc, sched, g["beta"], proximal.SolverOptions(line_search=g["line_search"]))
+        assert [s.newton_iters for s in rep.steps] == g["newton_iters"].tolist()
+        gm, gref = sum(s.gmres_total for s in rep.steps), int(g["gmres_iters"].sum())
+        assert abs(gm - gref) <= max(1, 0.01 * gref)
+        assert rel_err(rep.u, g["u"]) < 1e-9 and rel_err(rep.psi, g["psi"]) < 1e-9
