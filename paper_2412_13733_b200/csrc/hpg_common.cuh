@@ -30,6 +30,13 @@ constexpr double EXP_CLAMP = 700.0;   // hpgalerkin/assembly.py:25
 // a data-independent prologue) overlaps the previous kernel's tail; every
 // such kernel executes pdl_wait() before it touches memory written by
 // earlier work (a no-op for a kernel launched without the attribute).
+// 8-byte global -> shared copy, zero fill when !valid (src must still be a
+// mapped address)
+__device__ __forceinline__ void cp_async8z(double* dst, const double* src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 

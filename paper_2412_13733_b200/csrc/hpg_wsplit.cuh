@@ -186,10 +186,6 @@ __device__ __forceinline__ void ws_store_partial(const double (&Y)[NOUT][NT][NT]
           dst[(o * NP + 8 * at + 2 * c + j) * NP + 8 * bt + r] = Y[o][bt][at][j];
 }
 
-__device__ __forceinline__ void cp_async8z(double* dst, const double* src, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
-}
 
 // Stage the element's coefficient tiles of fields [f0, f0+nf) of MODE's field
 // list into dst (rows of n contiguous doubles), all threads of the CTA, as

@@ -69,8 +69,56 @@ def test_full_size_residual_and_apply(cfg_name, rule):
     assert orc.rel_err(y_cached, ry) < TOL
     assert orc.rel_err(y_psi, ry) < TOL
     b_u2, b_psi2, y2, _ = d.residual_apply_t(alpha, dev["psi_prev"], dev["u"], dev["psi"], dev["x"])
+    assert orc.rel_err(b_u2.cpu().numpy(), rb_u) < TOL
     assert orc.rel_err(b_psi2.cpu().numpy(), rb_psi) < TOL
     assert orc.rel_err(y2.cpu().numpy(), ry) < TOL
+    # without the weight cache (the single-pass low-degree kernels at config 4)
+    b_u3, b_psi3, flag3 = d.residual_t(alpha, dev["psi_prev"], dev["u"], dev["psi"])
+    assert orc.rel_err(b_u3.cpu().numpy(), rb_u) < TOL
+    assert orc.rel_err(b_psi3.cpu().numpy(), rb_psi) < TOL
+    if cfg.kind == "obstacle":
+        assert bool(flag3.item()) == rcl
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 6])
+@pytest.mark.parametrize("rule", ["gauss", "reference"])
+def test_low_degree_ragged_tiles(p, rule):
+    """Single-pass low-degree kernels (k_lowt tiles of 8 x 16 cells at p <= 3,
+    k_lowp above) on a rectangular, non-uniform 19 x 37 mesh: several tiles,
+    partial tiles on both edges, halo cells on every tile boundary, per-cell
+    sizes; residual, fused residual + apply and the clamp flag vs the oracle."""
+    import torch
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import Mesh1D, TensorMesh2D
+    from paper_2412_13733_b200.workloads import phi_sin
+    rng = np.random.default_rng(100 + p)
+    xs = np.concatenate([[0.0], np.cumsum(rng.uniform(0.5, 1.5, 19))]); xs /= xs[-1]
+    ys = np.concatenate([[0.0], np.cumsum(rng.uniform(0.5, 1.5, 37))]); ys /= ys[-1]
+    mesh = TensorMesh2D(Mesh1D(xs, np.full(19, p)), Mesh1D(ys, np.full(37, p)))
+    d = D.ObstacleDisc2D(mesh, 1.0, phi_sin, rule=rule, nq=p + 3 if rule == "gauss" else None)
+    t = d.tables
+    P = orc.Problem("obstacle", d.xpts, d.ypts, p, SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
+    psi = rng.standard_normal(d.ndof_psi)
+    psi[::97] = -800.0                            # clamped points: the flag must be raised
+    psi_prev = rng.standard_normal(d.ndof_psi)
+    u = rng.standard_normal(d.ndof_u)
+    x = rng.standard_normal(d.ndof_psi)
+    alpha = 3.0
+    phi_mom = P.data_moments(P.sample(phi_sin))
+    f_load = P.load_vector(P.sample(1.0))
+    rb_u, rb_psi, rcl = P.residual(alpha, psi_prev, u, psi, f_load, phi_moments=phi_mom)
+    ry = P.obstacle_apply_D(psi, x)
+    assert rcl
+    dv = {k: torch.from_numpy(v).cuda() for k, v in (("psi", psi), ("pp", psi_prev), ("u", u), ("x", x))}
+    b_u, b_psi, flag = d.residual_t(alpha, dv["pp"], dv["u"], dv["psi"])
+    assert orc.rel_err(b_u.cpu().numpy(), rb_u) < TOL
+    assert orc.rel_err(b_psi.cpu().numpy(), rb_psi) < TOL
+    assert bool(flag.item())
+    b_u2, b_psi2, y2, flag2 = d.residual_apply_t(alpha, dv["pp"], dv["u"], dv["psi"], dv["x"])
+    assert orc.rel_err(b_u2.cpu().numpy(), rb_u) < TOL
+    assert orc.rel_err(b_psi2.cpu().numpy(), rb_psi) < TOL
+    assert orc.rel_err(y2.cpu().numpy(), ry) < TOL
+    assert bool(flag2.item())
 
 
 @pytest.mark.parametrize("cfg_name", ["c1", "c2", "c4p4"])
