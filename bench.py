@@ -539,7 +539,7 @@ def gpu_config(cfg, rule, args, local, world, full, e2e_steps):
     traffic, traffic_src = NCU_TRAFFIC.get((cfg.name, rule), (None, "not captured for this config"))
     if cached:
         achieved = F_mv / t_kern / 1e12
-        roof = {"kernel": ("k_warp<NT,QT,M_OBST_CACHED>" if disc.plan.path == 0 else "k_cta<M_*_CACHED>")
+        roof = {"kernel": ("k_stream|k_warp<NT,QT,M_OBST_CACHED>" if disc.plan.path == 0 else "k_cta<M_*_CACHED>")
                           + " (Jacobian apply from cached weights)",
                 "bound": "tensor", "achieved": achieved, "peak": P_FP64_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / P_FP64_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,

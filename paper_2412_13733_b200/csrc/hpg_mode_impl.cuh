@@ -7,6 +7,7 @@
 #include "hpg_launch.cuh"
 #include "hpg_wsplit.cuh"
 #include "hpg_big.cuh"
+#include "hpg_stream.cuh"
 
 #ifndef HPG_WSPLIT_LIST
 #define HPG_WSPLIT_LIST
@@ -15,9 +16,51 @@
 namespace hpg {
 namespace {
 
+// many small cells, cached weights (config 1): the persistent streaming
+// kernel (hpg_stream.cuh), one CTA per SM
+template <int NT, int QT, int MODE>
+int launch_stream_t(const ElemArgs& A, int nsm, cudaStream_t s) {
+  using CF = StreamCfg<NT, QT, MODE>;
+  const size_t smem = sizeof(double) * (size_t)CF::SMEM_DBL;
+  struct Memo { size_t attr = 0; };
+  static PerDevice<Memo> memo;
+  cudaError_t se = memo.with([&](Memo& m) -> cudaError_t {
+    if (smem > m.attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_stream<NT, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      m.attr = smem;
+    }
+    return cudaSuccess;
+  });
+  if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_stream)", se);
+  cudaError_t e = launch_pdl(k_stream<NT, QT, MODE>, dim3(nsm), dim3(32 * CF::W), smem, s, A);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(HPG_ERR_CUDA, "k_stream launch", e);
+}
+
+inline int device_sm_count() {
+  struct Memo { int nsm = 0; };
+  static PerDevice<Memo> memo;
+  return memo.with([&](Memo& m) {
+    if (m.nsm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&m.nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return m.nsm;
+  });
+}
+
 template <int NT, int QT, int MODE>
 int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
   using TR = ModeTraits<MODE>;
+  if constexpr (MODE == M_OBST_CACHED && NT == 2 && QT <= 3) {
+    // every scheduler group of the persistent grid gets at least 2 MW cells
+    // (a cell then spans at most two warps' row-tile runs)
+    const bool stream_ok = getenv("HPG_NO_STREAM") == nullptr;
+    const int nsm = device_sm_count();
+    if (stream_ok && A.N / nsm / 4 >= 2 * StreamCfg<NT, QT, MODE>::MW) return launch_stream_t<NT, QT, MODE>(A, nsm, s);
+  }
   constexpr int NP = 8 * NT, QP = 8 * QT;
   constexpr int NSTAGE = WarpCfg<NT, QT, MODE>::REGX ? 0 : TR::NIN;
   using CF = WarpCfg<NT, QT, MODE>;

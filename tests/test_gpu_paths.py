@@ -120,3 +120,41 @@ def test_lowp_flag_and_nan_semantics(cfg_name, bad):
         assert np.array_equal(np.isnan(a), np.isnan(b))
         ok = ~np.isnan(a)
         assert orc.rel_err(a[ok], b[ok]) < TOL
+
+
+@pytest.mark.parametrize("ncx,ncy", [(64, 64), (61, 63), (59, 61)])
+def test_streaming_cached_apply(ncx, ncy):
+    """Config-1 shaped cached Jacobian apply on the persistent streaming
+    kernel (k_stream: equal row-tile runs per warp, cells split between two
+    warps summed through shared memory) vs the oracle and vs the one-wave
+    warp-per-cell kernel, on non-uniform meshes whose cells per SM are not a
+    multiple of the scheduler groups (every run-boundary case)."""
+    import torch
+    from types import SimpleNamespace
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import Mesh1D, TensorMesh2D
+    from paper_2412_13733_b200.workloads import phi_sin
+    p = 16
+    rng = np.random.default_rng(ncx * 100 + ncy)
+    xs = np.concatenate([[0.0], np.cumsum(rng.uniform(0.5, 1.5, ncx))]); xs /= xs[-1]
+    ys = np.concatenate([[0.0], np.cumsum(rng.uniform(0.5, 1.5, ncy))]); ys /= ys[-1]
+    mesh = TensorMesh2D(Mesh1D(xs, np.full(ncx, p)), Mesh1D(ys, np.full(ncy, p)))
+    d = D.ObstacleDisc2D(mesh, 1.0, phi_sin, rule="gauss", nq=24)
+    t = d.tables
+    P = orc.Problem("obstacle", d.xpts, d.ypts, p, SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
+    psi = 0.5 * rng.standard_normal(d.ndof_psi)
+    x = rng.standard_normal(d.ndof_psi)
+    tp, tx = torch.from_numpy(psi).cuda(), torch.from_numpy(x).cuda()
+    d.exp_moments_t(tp, wcache=True)
+
+    def run():
+        return d.apply_cached_t(tx).cpu().numpy()
+
+    y_stream = run()
+    y_stream2 = run()
+    y_wave = _with_env("HPG_NO_STREAM", run)
+    ry = P.obstacle_apply_D(psi, x)
+    assert np.array_equal(y_stream, y_stream2)          # deterministic
+    assert orc.rel_err(y_stream, ry) < TOL
+    assert orc.rel_err(y_wave, ry) < TOL
+    assert orc.rel_err(y_stream, y_wave) < 1e-13
