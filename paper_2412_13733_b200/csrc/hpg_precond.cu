@@ -27,7 +27,13 @@ namespace hpg {
 
 namespace {
 
-constexpr int LU_THREADS = 256;
+#ifndef HPG_LU_THREADS
+#define HPG_LU_THREADS 256
+#endif
+#ifndef HPG_LU_MINB
+#define HPG_LU_MINB 2
+#endif
+constexpr int LU_THREADS = HPG_LU_THREADS;
 constexpr int LU_UCH = 64;     // trailing-update column chunk
 constexpr int LU_ULD = 72;     // its smem row stride (conflict-free B fragments)
 constexpr int SOLVE_THREADS = 128;
@@ -95,7 +101,7 @@ __device__ __forceinline__ void argmax_combine(double& best, int& bi, double ov,
 }
 
 template <int KB>
-__global__ void __launch_bounds__(LU_THREADS, 2) k_lu(PrecArgs A) {
+__global__ void __launch_bounds__(LU_THREADS, HPG_LU_MINB) k_lu(PrecArgs A) {
   extern __shared__ double sm[];
   constexpr int LDP = KB + 1;
   constexpr int NOPIV = 0x7fffffff;

@@ -19,6 +19,8 @@ Two API levels:
 """
 
 import ctypes
+import os
+import weakref
 
 import numpy as np
 import torch
@@ -176,11 +178,16 @@ class _DeviceDisc:
     # direct.
     _STAGE_MIN = 1 << 17          # doubles (1 MB)
 
-    def _stage_buf(self, n):
+    _H2D_CHUNKS = int(os.environ.get("HPG_H2D_CHUNKS", "2"))   # measured: 2 beats 4 and 8 (per-chunk dispatch cost)
+
+    def _stage_buf(self, n, count=2):
         st = getattr(self, "_stage", None)
-        if st is None or st["n"] < n:
-            st = {"n": n, "buf": [torch.empty(n, dtype=F64, pin_memory=True) for _ in range(2)],
-                  "ev": [None, None]}
+        if st is None or st["n"] < n or len(st["buf"]) < count:
+            if st is not None:                       # both users keep fitting
+                n, count = max(n, st["n"]), max(count, len(st["buf"]))
+                torch.cuda.synchronize()
+            st = {"n": n, "buf": [torch.empty(n, dtype=F64, pin_memory=True) for _ in range(count)],
+                  "ev": [None] * count}
             self._stage = st
         return st
 
@@ -192,10 +199,16 @@ class _DeviceDisc:
         if n < self._STAGE_MIN:
             dev.copy_(torch.from_numpy(a))
             return dev
-        half = (n + 1) // 2
-        st = self._stage_buf(half)
+        # pipelined: the host copy of chunk i + 1 into its page-locked buffer
+        # overlaps the DMA of chunk i
+        nch = self._H2D_CHUNKS
+        step = (n + nch - 1) // nch
+        st = self._stage_buf(step, nch)
         at = torch.from_numpy(a)
-        for i, (lo, hi) in enumerate(((0, half), (half, n))):
+        for i in range(nch):
+            lo, hi = i * step, min(n, (i + 1) * step)
+            if lo >= hi:
+                break
             if st["ev"][i] is not None:
                 st["ev"][i].synchronize()          # the buffer's previous DMA is done
             st["buf"][i][:hi - lo].copy_(at[lo:hi])
@@ -205,14 +218,38 @@ class _DeviceDisc:
             st["ev"][i] = ev
         return dev
 
+    # Large results come back in page-locked memory of their own: the DMA
+    # writes the fresh array directly (no staging copy, no first-touch page
+    # faults of a new pageable block: 30.7 -> ~50 GB/s).  The block belongs to
+    # the returned array (its base keeps the tensor alive) and goes back to
+    # torch's caching host allocator when the caller drops the array.  Page-
+    # locked results still held by the caller are capped; beyond the cap the
+    # staged pageable path is used.
+    _PINNED_OUT_CAP = 4 << 30     # bytes
+    _pinned_out_bytes = 0
+
+    @classmethod
+    def _pinned_out_release(cls, nbytes):
+        cls._pinned_out_bytes -= nbytes
+
     def d2h(self, t, tag):
         """Device tensor -> fresh host array (the reference returns fresh arrays)."""
         t = t.reshape(-1)
         n = t.numel()
-        out = np.empty(n)
         if n < self._STAGE_MIN:
+            out = np.empty(n)
             torch.from_numpy(out).copy_(t)
             return out
+        cls = _DeviceDisc
+        if cls._pinned_out_bytes + 8 * n <= cls._PINNED_OUT_CAP and os.environ.get("HPG_NO_PINNED_OUT") is None:
+            buf = torch.empty(n, dtype=F64, pin_memory=True)
+            buf.copy_(t, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            out = buf.numpy()
+            cls._pinned_out_bytes += 8 * n
+            weakref.finalize(out, cls._pinned_out_release, 8 * n)
+            return out
+        out = np.empty(n)
         half = (n + 1) // 2
         st = self._stage_buf(half)
         ot = torch.from_numpy(out)
