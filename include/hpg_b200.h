@@ -90,6 +90,26 @@ int hpgGradientApplyD(hpgPlan plan, const double* psi, const double* phi,
  * (assembly.py:281-285) for the D of that psi. */
 int hpgApplyCached(hpgPlan plan, const double* wcache, const double* x,
                    double* y, void* stream);
+/* The same action restricted to the cells [cell_begin, cell_end) in x-major
+ * cell order (cell = cx * ncy + cy): reads / writes only those cells' tiles
+ * of x / y (full-length vectors).  D is block diagonal over cells
+ * (assembly.py:272-285, spaces.py:89-108), so a host-buffer caller pipelines
+ * slabs of cell columns (contiguous row ranges): upload, apply, download.
+ * HPG_ERR_UNSUPPORTED unless the plan applies cached weights on its
+ * warp-per-cell path (hpgPlanInfo path 0). */
+int hpgApplyCachedRange(hpgPlan plan, const double* wcache, const double* x,
+                        double* y, int cell_begin, int cell_end, void* stream);
+/* One slab of CellBlockMatrix @ x (assembly.py:281-285) with HOST buffers,
+ * the cell columns [cx_begin, cx_end): uploads the slab's rows of x from the
+ * page-locked `stage` (the slab's rows only, component after component) into
+ * the device vector dev_x on copy_stream, applies D on `stream` after the
+ * upload (hpgApplyCachedRange), and downloads the slab's rows of dev_y into
+ * the page-locked full-length y_host on `stream`.  Nothing waits on the
+ * host: the caller fills the next slab's stage buffer meanwhile and
+ * synchronises `stream` after the last slab. */
+int hpgApplyCachedHostSlab(hpgPlan plan, const double* wcache, const double* stage,
+                           double* dev_x, double* dev_y, double* y_host,
+                           int cx_begin, int cx_end, void* copy_stream, void* stream);
 
 /* proximal.residual (proximal.py:112-126), fused:
  *   b_u   = alpha f_load + B psi_prev - alpha A u - B psi

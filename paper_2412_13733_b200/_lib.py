@@ -28,6 +28,8 @@ SIGNATURES = {
     "hpgGradientMoments": [_P, _P, _P, _P, _P, _P],
     "hpgGradientApplyD": [_P, _P, _P, _P, _P, _P],
     "hpgApplyCached": [_P, _P, _P, _P, _P],
+    "hpgApplyCachedRange": [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P],
+    "hpgApplyCachedHostSlab": [_P, _P, _P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P],
     "hpgResidual": [_P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "hpgResidualApply": [_P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "hpgBlocks": [_P, _P, _P, _I, _I, _P],

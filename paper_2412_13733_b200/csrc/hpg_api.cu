@@ -85,6 +85,9 @@ struct hpgPlan_st {
   bool concurrent = false;
   cudaStream_t aux[1] = {nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[1] = {nullptr};
+  // hpgApplyCachedHostSlab: upload-done events, round robin (created on first use)
+  cudaEvent_t ev_slab[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int ev_slab_next = 0;
   double* mscr = nullptr;       // psi-side moments [ndof_psi]
   double* wscr = nullptr;       // weight cache of the fused residual + cached apply
   // weight cache written by the LAST kernel of this plan's most recent call
@@ -400,6 +403,8 @@ int hpgPlanDestroy(hpgPlan P) {
   if (P->aux[0]) cudaStreamDestroy(P->aux[0]);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join[0]) cudaEventDestroy(P->ev_join[0]);
+  for (cudaEvent_t e : P->ev_slab)
+    if (e) cudaEventDestroy(e);
   delete P;
   return HPG_OK;
 }
@@ -490,6 +495,62 @@ int hpgApplyCached(hpgPlan P, const double* wcache, const double* x, double* y, 
   A.wc_early = early_ok && prev_wc != wcache;
   if (P->kind == HPG_OBSTACLE) return run_elem<M_OBST_CACHED>(P, A, (cudaStream_t)stream);
   return run_elem<M_GRAD_CACHED>(P, A, (cudaStream_t)stream);
+}
+
+// Cached apply restricted to the cells [cell_begin, cell_end) (x-major cell
+// order: a range of whole cell columns is a contiguous row range of x and y).
+// The apply is cell-local (spaces.py:89-108), so a host caller can pipeline
+// slabs: upload slab k while slab k - 1 is applied and slab k - 2 downloaded.
+int hpgApplyCachedRange(hpgPlan P, const double* wcache, const double* x, double* y, int cell_begin,
+                        int cell_end, void* stream) {
+  HPG_NVTX("hpgApplyCachedRange");
+  const double* prev_wc = P ? P->last_wc : nullptr;
+  if (int rc = check(P)) return rc;
+  if (!wcache || !x || !y) return fail(HPG_ERR_ARG, "null pointer");
+  if (cell_begin < 0 || cell_end > P->N || cell_begin > cell_end) return fail(HPG_ERR_ARG, "bad cell range");
+  const int mode = P->kind == HPG_OBSTACLE ? M_OBST_CACHED : M_GRAD_CACHED;
+  if (P->path[mode] != PATH_WARP) return fail(HPG_ERR_UNSUPPORTED, "cell ranges need the warp-per-cell apply path");
+  if (cell_begin == cell_end) return HPG_OK;
+  ElemArgs A = base_args(P);
+  A.wc_in = wcache; A.in1 = x; A.out = y;
+  A.e0 = cell_begin; A.N = cell_end;
+  static const bool early_ok = getenv("HPG_NO_EARLY_WC") == nullptr;
+  A.wc_early = early_ok && prev_wc != wcache;
+  if (P->kind == HPG_OBSTACLE) return run_elem<M_OBST_CACHED>(P, A, (cudaStream_t)stream);
+  return run_elem<M_GRAD_CACHED>(P, A, (cudaStream_t)stream);
+}
+
+// One slab (cell columns [cx_begin, cx_end)) of a host-buffer D @ x:
+//   upload  stage -> dev_x   on copy_stream   (stage: page-locked, the slab's
+//                                              rows, component after component)
+//   apply   dev_x -> dev_y   on stream, after the upload
+//   download dev_y -> y_host on stream        (y_host: page-locked, full length)
+// The caller fills `stage` for slab k + 1 while slab k is in flight and
+// synchronises `stream` once at the end; uploads (copy_stream) and downloads
+// (stream) of neighbouring slabs use both PCIe directions at once.
+int hpgApplyCachedHostSlab(hpgPlan P, const double* wcache, const double* stage, double* dev_x, double* dev_y,
+                           double* y_host, int cx_begin, int cx_end, void* copy_stream, void* stream) {
+  HPG_NVTX("hpgApplyCachedHostSlab");
+  if (P == nullptr) return fail(HPG_ERR_ARG, "null plan");
+  if (!wcache || !stage || !dev_x || !dev_y || !y_host) return fail(HPG_ERR_ARG, "null pointer");
+  if (cx_begin < 0 || cx_end > P->ncx || cx_begin >= cx_end) return fail(HPG_ERR_ARG, "bad cell-column range");
+  cudaStream_t up = (cudaStream_t)copy_stream, s = (cudaStream_t)stream;
+  const int ncmp = P->kind == HPG_OBSTACLE ? 1 : 2;
+  const size_t rows = (size_t)P->n * P->ncy * P->n;            // doubles per cell column and component
+  const size_t ln = (size_t)(cx_end - cx_begin) * rows;
+  for (int c = 0; c < ncmp; ++c)
+    CUDA_TRY(cudaMemcpyAsync(dev_x + c * P->ncomp + cx_begin * rows, stage + c * ln, sizeof(double) * ln,
+                             cudaMemcpyHostToDevice, up));
+  cudaEvent_t& ev = P->ev_slab[P->ev_slab_next];
+  P->ev_slab_next = (P->ev_slab_next + 1) % 8;
+  if (ev == nullptr) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ev, up));
+  CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
+  if (int rc = hpgApplyCachedRange(P, wcache, dev_x, dev_y, cx_begin * P->ncy, cx_end * P->ncy, stream)) return rc;
+  for (int c = 0; c < ncmp; ++c)
+    CUDA_TRY(cudaMemcpyAsync(y_host + c * P->ncomp + cx_begin * rows, dev_y + c * P->ncomp + cx_begin * rows,
+                             sizeof(double) * ln, cudaMemcpyDeviceToHost, s));
+  return HPG_OK;
 }
 
 // U side of the residual: b_psi <- phi_mom - B^T u (obstacle) | -B^T u

@@ -107,6 +107,8 @@ struct ElemArgs {
   double* edge;      // [N][4m-4] hat-involved local contributions
   int usmem;         // doubles of U-side shared memory per thread group
   double* ubuf;      // CTA path, large m: U-side buffers in global scratch [N][usmem]
+  int e0;            // warp / streaming cached apply: first cell of the range
+                     // [e0, N) (hpgApplyCachedRange); 0 everywhere else
   int wc_early;      // cached apply: the weight cache was not written by the
                      // immediately preceding kernel, so it may be prefetched
                      // before griddepcontrol.wait (hpgApplyCached decides)

@@ -273,7 +273,7 @@ k_warp(ElemArgs A) {
     }
   };
   const int stride = gridDim.x * W;
-  int e = blockIdx.x * W + warp;
+  int e = A.e0 + blockIdx.x * W + warp;
   if (A.wc_early && e < A.N) load_weights(e, 0);
   // one wave: let the next kernel in the stream start its prologue now --
   // except a kernel writing a weight cache (see above)

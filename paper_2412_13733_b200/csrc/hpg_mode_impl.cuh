@@ -59,7 +59,7 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
     // (a cell then spans at most two warps' row-tile runs)
     const bool stream_ok = getenv("HPG_NO_STREAM") == nullptr;
     const int nsm = device_sm_count();
-    if (stream_ok && A.N / nsm / 4 >= 2 * StreamCfg<NT, QT, MODE>::MW) return launch_stream_t<NT, QT, MODE>(A, nsm, s);
+    if (stream_ok && (A.N - A.e0) / nsm / 4 >= 2 * StreamCfg<NT, QT, MODE>::MW) return launch_stream_t<NT, QT, MODE>(A, nsm, s);
   }
   constexpr int NP = 8 * NT, QP = 8 * QT;
   constexpr int NSTAGE = WarpCfg<NT, QT, MODE>::REGX ? 0 : TR::NIN;
@@ -91,7 +91,7 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
     return cudaSuccess;
   });
   if (se != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_warp)", se);
-  int need = (A.N + W * CF::CPW - 1) / (W * CF::CPW);
+  int need = (A.N - A.e0 + W * CF::CPW - 1) / (W * CF::CPW);
   int grid = need < grid_cap ? need : grid_cap;
   // programmatic dependent launch: the table prologue overlaps the previous
   // kernel's tail (k_warp orders its data reads with griddepcontrol.wait)

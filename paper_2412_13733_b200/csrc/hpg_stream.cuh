@@ -95,10 +95,10 @@ k_stream(ElemArgs A) {
 
   // CTA b owns cells b, b + grid, ...; its k-th cell goes to group k mod 4;
   // the group's row tiles [lo, hi) (cell-major) are this warp's run
-  const int K = ((int)A.N - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int K = ((int)A.N - A.e0 - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const int C = (K - g + 3) / 4;
   const int lo = (m * QT * C) / MW, hi = ((m + 1) * QT * C) / MW;
-  auto cell_of = [&](int i) { return (int)blockIdx.x + (g + 4 * i) * (int)gridDim.x; };
+  auto cell_of = [&](int i) { return A.e0 + (int)blockIdx.x + (g + 4 * i) * (int)gridDim.x; };
   int i = lo / QT;
   const int i_end = (hi + QT - 1) / QT;
 

@@ -171,14 +171,18 @@ class _DeviceDisc:
         return b[:n]
 
     # Host<->device transfers of the reference-facing API.  Measured on the
-    # B200 boxes (tools/xfer_bench2.py, 7.4 MB): a direct pageable copy runs
-    # at 17.7 GB/s H2D / 14.5 GB/s D2H; staging through two pinned half-size
-    # buffers -- a multi-threaded host copy (torch) of one half overlapping
-    # the DMA of the other -- reaches 41.5 / 30.7 GB/s.  Small vectors go
-    # direct.
+    # B200 boxes (tools/xfer_bench2.py, tools/e2e_slab_probe.py, 7.4 MB): a
+    # direct pageable copy runs at 17.7 GB/s H2D / 14.5 GB/s D2H; one DMA from
+    # / to page-locked memory at 54 GB/s (0.137 ms), both directions at once
+    # at 0.153 ms.  The multi-threaded host copy (torch) into the page-locked
+    # staging buffer runs at 53 GB/s when the source is not cache resident, so
+    # uploads stage through two half-size buffers (the copy of one half
+    # overlapping the DMA of the other: 0.22 ms; one chunk 0.28, four 0.27,
+    # eight 0.44 -- every extra DMA / event costs ~20 us on these boxes).
+    # Small vectors go direct.
     _STAGE_MIN = 1 << 17          # doubles (1 MB)
 
-    _H2D_CHUNKS = int(os.environ.get("HPG_H2D_CHUNKS", "2"))   # measured: 2 beats 4 and 8 (per-chunk dispatch cost)
+    _H2D_CHUNKS = int(os.environ.get("HPG_H2D_CHUNKS", "2"))
 
     def _stage_buf(self, n, count=2):
         st = getattr(self, "_stage", None)
@@ -267,6 +271,55 @@ class _DeviceDisc:
             ot[lo:hi].copy_(st["buf"][i][:hi - lo])
             st["ev"][i] = None
         return out
+
+    # D @ x with host buffers, pipelined over slabs of cell columns.  D is
+    # block diagonal over cells and a slab of whole cell columns is a
+    # contiguous row range of the x-major vectors, so slab k uploads (copy
+    # stream) while slab k - 1 is applied and downloaded (compute stream):
+    # both PCIe directions are busy at once, and the result lands directly in
+    # a page-locked array of its own (see d2h).
+    _SLABS = int(os.environ.get("HPG_MATVEC_SLABS", "2"))   # c1, per D @ x: 2 slabs 0.41 ms, 1: 0.43, 3: 0.41, 4: 0.50
+
+    def host_matvec_cached(self, x, wcache):
+        a = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        n = a.size
+        self._check_len(torch.from_numpy(a), self.ndof_psi, "x")
+        cls = _DeviceDisc
+        S = min(self._SLABS, self.ncx)
+        if (S < 2 or n < 2 * self._STAGE_MIN or self.plan.path != 0
+                or cls._pinned_out_bytes + 8 * n > cls._PINNED_OUT_CAP
+                or os.environ.get("HPG_NO_PINNED_OUT") is not None):
+            y = self.apply_cached_t(self.h2d(a, "x"), out=self._dev("out_y", n), wcache=wcache)
+            return self.d2h(y, "y")
+        dev_x, dev_y = self._dev("in_x", n), self._dev("out_y", n)
+        out = torch.empty(n, dtype=F64, pin_memory=True)
+        cur = torch.cuda.current_stream()
+        up = getattr(self, "_up_stream", None)
+        if up is None:
+            up = self._up_stream = torch.cuda.Stream()
+        up.wait_stream(cur)                    # earlier readers of dev_x are done
+        at = torch.from_numpy(a)
+        rows = self.n * self.ncy * self.n      # doubles per cell column and component
+        bounds = [self.ncx * k // S for k in range(S + 1)]
+        st = self._stage_buf(max(bounds[k + 1] - bounds[k] for k in range(S)) * rows * self.ncomp, S)
+        for k in range(S):
+            cx0, cx1 = bounds[k], bounds[k + 1]
+            ln = (cx1 - cx0) * rows
+            # uploads of an earlier call of this method finished before it
+            # returned; h2d() shares the buffers and leaves an event behind
+            if st["ev"][k] is not None:
+                st["ev"][k].synchronize()
+                st["ev"][k] = None
+            for c in range(self.ncomp):
+                lo = c * self.ncomp_dofs + cx0 * rows
+                st["buf"][k][c * ln:(c + 1) * ln].copy_(at[lo:lo + ln])
+            _lib.call("hpgApplyCachedHostSlab", self.plan.handle, _vp(wcache), _vp(st["buf"][k]), _vp(dev_x),
+                      _vp(dev_y), _vp(out), cx0, cx1, ctypes.c_void_p(up.cuda_stream), _stream())
+        cur.synchronize()
+        res = out.numpy()
+        cls._pinned_out_bytes += 8 * n
+        weakref.finalize(res, cls._pinned_out_release, 8 * n)
+        return res
 
     def _check_len(self, v, n, what):
         if v.numel() != n:
@@ -632,9 +685,7 @@ class DeviceCellBlockMatrix:
         return self.disc.blocks_matvec_t(self.blocks_t(), x_t, out=out)
 
     def matvec(self, x):
-        d = self.disc
-        y = self.matvec_t(d.h2d(x, "x"), out=d._dev("out_y", self.n))
-        return d.d2h(y, "y")
+        return self.disc.host_matvec_cached(x, self._w)
 
     def tocsc(self):
         import scipy.sparse as sp
