@@ -362,6 +362,294 @@ __global__ void __launch_bounds__(LU_THREADS, HPG_LU_MINB) k_lu(PrecArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// Row-per-thread LU for 32 < nb <= 256 (config 1: 225): the same LAPACK getrf
+// arithmetic as k_lu, reorganised so that no row ever moves during the
+// factorisation.
+//  * Thread t owns storage row t.  A panel's 32 entries of the row live in
+//    REGISTERS; the column loop is fully unrolled: block argmax of |a_j| over
+//    the still-active rows (ties: smallest LAPACK position, idamax), the
+//    winner publishes its row through shared memory, every active row scales
+//    and rank-1 updates its registers.  Two barriers per column and no
+//    shared-memory row traffic.
+//  * Implicit pivoting: a pivot row retires in place.  Each row tracks the
+//    position LAPACK's explicit interchanges would have given it (ipiv and
+//    tie-breaking are exactly getrf's), the trailing update runs over the
+//    compacted list of active rows, U12 over the panel's pivot rows.  The
+//    per-panel row interchanges of the right and left parts (k_lu's gather
+//    phase) are replaced by ONE permuting pass at the end.
+// (P_e = -D_e - T/alpha - beta E_e is formed by k_precond_transform first.)
+constexpr int LU2_T = 256, LU2_KB = 32, LU2_LDP = 33;
+
+size_t lu2_smem(int nb) {
+  return sizeof(double) * ((size_t)nb * LU2_LDP + LU2_KB * LU2_LDP + 2 * LU2_KB * LU_ULD + LU2_KB + 2) +
+         sizeof(int) * (4 * 8 + 2 + LU2_KB + 2 * LU2_T + 16);
+}
+
+// U12 = Linv A12 on the panel's pivot rows and A22 -= L21 U12 on the active
+// rows, per 64-column chunk, on the FP64 tensor cores.  Its own function (not
+// inlined) so its registers are allocated independently of the column loop's.
+__device__ __noinline__ void lu2_trailing(double* __restrict__ M, int nb, int k0, int kb, const double* sP,
+                                          const double* sLi, double* sA, double* sU, const int* sPivT,
+                                          const int* sAct) {
+  // (72-column chunks -- 13 instead of 16 chunk passes per 225-wide block --
+  // measured equal: the pass is bound by the trailing matrix's HBM round trip)
+  constexpr int KB = LU2_KB, LDP = LU2_LDP, NW = LU2_T / 32, CW = LU_UCH, CT = CW / 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = lane >> 2, c = lane & 3;
+      const int nact = nb - (k0 + kb);
+      const int nrt = (nact + 7) >> 3;
+      for (int cc0 = k0 + kb; cc0 < nb; cc0 += CW) {
+#pragma unroll 4
+        for (int idx = tid; idx < KB * CW; idx += LU2_T) {
+          const int j = idx / CW, t = idx - (idx / CW) * CW;
+          const int col = cc0 + t;
+          double v = 0.0;
+          if (j < kb && col < nb) {
+            const int row = sPivT[j];
+            v = M[(size_t)row * nb + col];
+          }
+          sA[j * LU_ULD + t] = v;
+        }
+        __syncthreads();
+        for (int tile = warp; tile < (KB / 8) * CT; tile += NW) {
+          const int mt = tile / CT, nt = tile - mt * CT;
+          double u[2] = {0.0, 0.0};
+#pragma unroll
+          for (int ks = 0; ks < KB / 4; ++ks)
+            dmma(u, sLi[(8 * mt + r) * LDP + 4 * ks + c], sA[(4 * ks + c) * LU_ULD + 8 * nt + r]);
+          const int row = 8 * mt + r, col = 8 * nt + 2 * c;
+          sU[row * LU_ULD + col] = u[0];
+          sU[row * LU_ULD + col + 1] = u[1];
+          if (row < kb) {
+            double* mrow = M + (size_t)sPivT[row] * nb;
+            if (cc0 + col < nb) mrow[cc0 + col] = u[0];
+            if (cc0 + col + 1 < nb) mrow[cc0 + col + 1] = u[1];
+          }
+        }
+        __syncthreads();
+        for (int rt = warp; rt < nrt; rt += NW) {
+          const bool rv = 8 * rt + r < nact;
+          const int row = sAct[rv ? 8 * rt + r : 0];
+          double* mrow = M + (size_t)row * nb;
+          double acc[CT][2];
+#pragma unroll
+          for (int nt = 0; nt < CT; ++nt) {
+            const int col = cc0 + 8 * nt + 2 * c;
+            acc[nt][0] = (rv && col < nb) ? mrow[col] : 0.0;
+            acc[nt][1] = (rv && col + 1 < nb) ? mrow[col + 1] : 0.0;
+          }
+#pragma unroll
+          for (int ks = 0; ks < KB / 4; ++ks) {
+            const double al = rv ? -sP[row * LDP + 4 * ks + c] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < CT; ++nt) dmma(acc[nt], al, sU[(4 * ks + c) * LU_ULD + 8 * nt + r]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < CT; ++nt) {
+            const int col = cc0 + 8 * nt + 2 * c;
+            if (rv && col < nb) mrow[col] = acc[nt][0];
+            if (rv && col + 1 < nb) mrow[col + 1] = acc[nt][1];
+          }
+        }
+        __syncthreads();
+      }
+}
+
+__global__ void __launch_bounds__(LU2_T, 2) k_lu2(PrecArgs A) {
+  extern __shared__ double sm[];
+  constexpr int KB = LU2_KB, LDP = LU2_LDP, NW = LU2_T / 32;
+  const int nb = A.nb;
+  double* sP = sm;                                  // panel rows by storage row [nb][LDP]
+  double* sLi = sP + (size_t)nb * LDP;              // L11^{-1} [KB][LDP]
+  double* sA = sLi + KB * LDP;                      // A12 chunk [KB][LU_ULD]
+  double* sU = sA + KB * LU_ULD;                    // U12 chunk [KB][LU_ULD]
+  double* sRow = sU + KB * LU_ULD;                  // the pivot row, broadcast [KB]
+  unsigned* sSh = reinterpret_cast<unsigned*>(sRow + KB + 2);   // (sRow[KB]: 1 / pivot) per-warp argmax key halves [8]
+  unsigned* sSl = sSh + 8;
+  int* sSp = reinterpret_cast<int*>(sSl + 8);       // ... LAPACK positions [8]
+  int* sSt = sSp + 8;                               // ... storage rows [8]
+  int* sPosJ = sSt + 8;                             // storage row currently at position k0 + j [2]
+  int* sPivT = sPosJ + 2;                           // storage rows of the panel's pivots [KB]
+  int* sAct = sPivT + KB;                           // compacted active storage rows [LU2_T]
+  int* sFpos = sAct + LU2_T;                        // final position per storage row, -1 while active [LU2_T]
+  int* sCnt = sFpos + LU2_T;                        // per-warp active counts [8] (+ total)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = lane >> 2, c = lane & 3;
+  long long t_last = clock64();
+  int ph_last = 7;
+
+  for (int cl = blockIdx.x; cl < A.count; cl += gridDim.x) {
+    double* M = A.M + (size_t)cl * nb * nb;
+    int* piv = A.ipiv + (size_t)cl * nb;
+    int pos = tid;                   // LAPACK position of this thread's row
+    int fpos = -1;                   // its final position once it has been a pivot
+    bool active = tid < nb;
+    sFpos[tid] = -1;
+    __syncthreads();
+    for (int k0 = 0; k0 < nb; k0 += KB) {
+      const int kb = nb - k0 < KB ? nb - k0 : KB;
+      PROF_MARK(0);
+      // (1) panel -> shared memory (coalesced) -> the owning thread's registers
+      bool bad = false;
+#pragma unroll 4
+      for (int idx = tid; idx < nb * KB; idx += LU2_T) {
+        const int i = idx >> 5, j = idx & 31;
+        double v = 0.0;
+        if (j < kb && sFpos[i] < 0) {
+          v = M[(size_t)i * nb + k0 + j];
+          bad |= !isfinite(v);
+        }
+        sP[i * LDP + j] = v;
+      }
+      if (bad && A.info) atomicOr(A.info, 1);
+      __syncthreads();
+      double a[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) a[j] = active ? sP[tid * LDP + j] : 0.0;
+      PROF_MARK(7);
+      // (2) the panel's columns
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        if (j < kb) {                                  // block-uniform
+          // idamax over the active rows: key = bits(|a_j|) + 1 (order
+          // preserving for non-negative doubles), 0 for a retired row or a
+          // NaN (never wins); ties go to the smallest LAPACK position.
+          // Hardware warp reductions (REDUX) on the key's halves, then on the
+          // position.
+          const double av = fabs(a[j]);
+          const unsigned long long key = (active && av == av) ? (unsigned long long)__double_as_longlong(av) + 1ull : 0ull;
+          unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+          unsigned mhi = __reduce_max_sync(~0u, hi);
+          unsigned mlo = __reduce_max_sync(~0u, hi == mhi ? lo : 0u);
+          int cand = (hi == mhi && lo == mlo) ? pos : 0x7fffffff;
+          int bp = __reduce_min_sync(~0u, cand);
+          if (cand == bp) { sSh[warp] = mhi; sSl[warp] = mlo; sSp[warp] = bp; sSt[warp] = tid; }
+          if (active && pos == k0 + j) sPosJ[j & 1] = tid;
+          __syncthreads();
+          hi = lane < NW ? sSh[lane] : 0u;
+          lo = lane < NW ? sSl[lane] : 0u;
+          const int wp = lane < NW ? sSp[lane] : 0x7fffffff, wt = lane < NW ? sSt[lane] : 0x7fffffff;
+          mhi = __reduce_max_sync(~0u, hi);
+          mlo = __reduce_max_sync(~0u, hi == mhi ? lo : 0u);
+          cand = (hi == mhi && lo == mlo) ? wp : 0x7fffffff;
+          bp = __reduce_min_sync(~0u, cand);
+          int bt = __reduce_min_sync(~0u, cand == bp ? wt : 0x7fffffff);
+          if ((mhi | mlo) == 0u) { bt = sPosJ[j & 1]; bp = k0 + j; }   // all-NaN column: no interchange
+          if (tid == bt) {
+#pragma unroll
+            for (int cc = j; cc < KB; ++cc) sRow[cc] = a[cc];
+            // 1 / pivot when that is safe (dgetrf2's sfmin rule), else 0: divide
+            sRow[KB] = (a[j] != 0.0 && fabs(a[j]) >= DBL_MIN) ? 1.0 / a[j] : 0.0;
+            sPivT[j] = tid;
+            piv[k0 + j] = bp;
+            active = false;
+            fpos = k0 + j;
+          } else if (active && pos == k0 + j) {
+            pos = bp;                                  // getrf's interchange of positions k0 + j and bp
+          }
+          __syncthreads();
+          const double pv = sRow[j];
+          if (pv == 0.0 && tid == 0 && A.info) atomicOr(A.info, 2);
+          if (active) {
+            double l = a[j];
+            const double rp = sRow[KB];
+            if (rp != 0.0) l *= rp;
+            else if (pv != 0.0) l /= pv;
+            a[j] = l;
+#pragma unroll
+            for (int cc = j + 1; cc < KB; ++cc) a[cc] -= l * sRow[cc];
+          }
+        }
+      }
+      PROF_MARK(1);
+      // (3) the panel back to shared memory (trailing-update operand) and to
+      //     global memory; the active list
+      const bool mine = tid < nb && (fpos < 0 || fpos >= k0);
+      if (mine) {
+#pragma unroll
+        for (int j = 0; j < KB; ++j) sP[tid * LDP + j] = a[j];
+      }
+      sFpos[tid] = tid < nb ? fpos : 0;
+      {
+        const unsigned bal = __ballot_sync(~0u, active);
+        if (lane == 0) sCnt[warp] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+        for (int w = 0; w < warp; ++w) off += sCnt[w];
+        if (active) sAct[off + __popc(bal & ((1u << lane) - 1))] = tid;
+      }
+#pragma unroll 4
+      for (int idx = tid; idx < nb * KB; idx += LU2_T) {
+        const int i = idx >> 5, j = idx & 31;
+        const int fp = sFpos[i];
+        if (j < kb && (fp < 0 || fp >= k0)) M[(size_t)i * nb + k0 + j] = sP[i * LDP + j];
+      }
+      PROF_MARK(3);
+      // (4) Linv = L11^{-1} (unit lower; L11 = the pivot rows in pivot order)
+      double* sL11 = sA;                              // [KB][LDP], zero beyond kb (sA is free here)
+      for (int idx = tid; idx < KB * KB; idx += LU2_T) {
+        const int i = idx >> 5, j = idx & 31;
+        sL11[i * LDP + j] = (i < kb && j < i) ? sP[sPivT[i] * LDP + j] : 0.0;
+      }
+      __syncthreads();
+      if (tid < KB) {
+        // column cc of L11^{-1}: t = e_cc, then t_i -= L_ij t_j for j < i in
+        // axpy order -- straight-line, every t_j final before it is used
+        const int cc = tid;
+        double t[KB];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) t[i] = i == cc ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < KB - 1; ++j)
+#pragma unroll
+          for (int i = j + 1; i < KB; ++i) t[i] -= sL11[i * LDP + j] * t[j];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) sLi[i * LDP + cc] = (i < kb && cc < kb) ? t[i] : 0.0;
+      }
+      __syncthreads();
+      PROF_MARK(4);
+      // (5) per 64-column chunk: U12 = Linv A12 (pivot rows), A22 -= L21 U12
+      //     (active rows), both on the FP64 tensor cores
+      lu2_trailing(M, nb, k0, kb, sP, sLi, sA, sU, sPivT, sAct);
+      PROF_MARK(5);
+    }
+    PROF_MARK(6);
+    // (6) rows to their LAPACK positions: 32 columns of every row through
+    //     shared memory at a time (all loads of a column block before its stores)
+    for (int cb = 0; cb < nb; cb += KB) {
+#pragma unroll 4
+      for (int idx = tid; idx < nb * KB; idx += LU2_T) {
+        const int i = idx >> 5, j = idx & 31;
+        if (cb + j < nb) sP[i * LDP + j] = M[(size_t)i * nb + cb + j];
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int idx = tid; idx < nb * KB; idx += LU2_T) {
+        const int i = idx >> 5, j = idx & 31;
+        if (cb + j < nb) M[(size_t)sFpos[i] * nb + cb + j] = sP[i * LDP + j];
+      }
+      __syncthreads();
+    }
+    if (A.perm != nullptr && tid < nb) A.perm[(size_t)cl * nb + fpos] = tid;
+    PROF_MARK(2);
+    __syncthreads();
+  }
+}
+
+int launch_lu2(const PrecArgs& A, int nsm, cudaStream_t s) {
+  const size_t smem = lu2_smem(A.nb);
+  cudaError_t e = cudaFuncSetAttribute(k_lu2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_lu2)", e);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lu2, LU2_T, smem);
+  const long long cap = (long long)nsm * (occ > 0 ? occ : 1);
+  const int grid = (int)(A.count < cap ? A.count : cap);
+  k_lu2<<<grid, LU2_T, smem, s>>>(A);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? HPG_OK : set_error(HPG_ERR_CUDA, "k_lu2 launch", e);
+}
+
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(SOLVE_THREADS, 8) k_lu_solve(ElemArgs E, const double* __restrict__ lu,
                                                             const int* __restrict__ ipiv,
                                                             const int* __restrict__ perm, int nb,
@@ -692,6 +980,16 @@ int launch_lu(const PrecArgs& A, int nsm, cudaStream_t s) {
   if (A.nb <= 8) return launch_lu_warp_t<8>(A, nsm, s);
   if (A.nb <= 16) return launch_lu_warp_t<16>(A, nsm, s);
   if (A.nb <= 32) return launch_lu_warp_t<32>(A, nsm, s);
+  // one row per thread, implicit pivoting (config 1)
+  if (A.nb <= LU2_T && getenv("HPG_LU2_OFF") == nullptr) {
+    if (A.transform) {
+      int rc = launch_precond_transform(A, s);
+      if (rc) return rc;
+    }
+    PrecArgs B = A;
+    B.transform = 0;
+    return launch_lu2(B, nsm, s);
+  }
   // widest panel that fits shared memory (HPG_LU_KB overrides, for tuning)
   int kb = 32;
   if (const char* env = getenv("HPG_LU_KB")) kb = atoi(env);
