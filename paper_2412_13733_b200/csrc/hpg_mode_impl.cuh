@@ -257,6 +257,9 @@ int launch_big_t(ElemArgs A, cudaStream_t s) {
       int nclusters = 0;
       cudaError_t qe = cudaOccupancyMaxActiveClusters(&nclusters, k_big<MODE, NT, QT, RB, W>, &q);
       if (qe == cudaSuccess && nclusters >= A.N) m.ok_res = 1;
+      if (getenv("HPG_DEBUG"))
+        fprintf(stderr, "[hpg] k_big mode %d: %d cells x %d splits, smem %zu: max active clusters %d (%s) -> %s\n",
+                MODE, A.N, A.splits, smem, nclusters, cudaGetErrorString(qe), m.ok_res ? "cluster" : "reduce kernel");
       cudaGetLastError();
     }
     A.cluster_red = try_cluster ? m.ok_res : 0;

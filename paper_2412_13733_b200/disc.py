@@ -180,7 +180,10 @@ class _DeviceDisc:
     # overlapping the DMA of the other: 0.22 ms; one chunk 0.28, four 0.27,
     # eight 0.44 -- every extra DMA / event costs ~20 us on these boxes).
     # Small vectors go direct.
-    _STAGE_MIN = 1 << 17          # doubles (1 MB)
+    _STAGE_MIN = 1 << 17          # doubles (1 MB): uploads below go direct (pageable)
+    _CHUNK_MIN = 1 << 19          # doubles (4 MB): uploads below stage as one chunk
+    _PIN_OUT_MIN = 1 << 14        # doubles (128 KB): results below come back pageable
+                                  # (c3's 0.84 MB vector: direct 0.086 ms, page-locked 0.048 ms)
 
     _H2D_CHUNKS = int(os.environ.get("HPG_H2D_CHUNKS", "2"))
 
@@ -205,7 +208,7 @@ class _DeviceDisc:
             return dev
         # pipelined: the host copy of chunk i + 1 into its page-locked buffer
         # overlaps the DMA of chunk i
-        nch = self._H2D_CHUNKS
+        nch = self._H2D_CHUNKS if n >= self._CHUNK_MIN else 1
         step = (n + nch - 1) // nch
         st = self._stage_buf(step, nch)
         at = torch.from_numpy(a)
@@ -236,11 +239,70 @@ class _DeviceDisc:
     def _pinned_out_release(cls, nbytes):
         cls._pinned_out_bytes -= nbytes
 
+    def h2d_many(self, arrs, tags):
+        """Several host arrays -> device tensors.  Small / mid-size arrays
+        (each below the chunking threshold) are packed into one page-locked
+        staging buffer and uploaded by ONE DMA into one device buffer (the
+        results are 256-byte aligned views of it); large ones go one by one
+        through the pipelined path."""
+        flat = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in arrs]
+        if any(a.size >= self._CHUNK_MIN for a in flat) or sum(a.size for a in flat) < 64:
+            return [self.h2d(a, t) for a, t in zip(flat, tags)]
+        offs, total = [], 0
+        for a in flat:
+            offs.append(total)
+            total += (a.size + 31) // 32 * 32
+        st = self._stage_buf(total, 1)
+        if st["ev"][0] is not None:
+            st["ev"][0].synchronize()
+        pin = st["buf"][0]
+        for a, o in zip(flat, offs):
+            if a.size:
+                pin[o:o + a.size].copy_(torch.from_numpy(a))
+        dev = self._dev("in_many_" + "_".join(tags), total)
+        dev.copy_(pin[:total], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        st["ev"][0] = ev
+        return [dev[o:o + a.size] for a, o in zip(flat, offs)]
+
+    def d2h_many(self, tensors, flag=None):
+        """Several device tensors -> fresh host arrays with ONE stream
+        synchronisation (page-locked results enqueued back to back); ``flag``
+        (a device int tensor) comes back as a Python int the same way."""
+        cls = _DeviceDisc
+        outs, pend = [], []
+        for t in tensors:
+            t = t.reshape(-1)
+            n = t.numel()
+            if (n >= self._PIN_OUT_MIN and cls._pinned_out_bytes + 8 * n <= cls._PINNED_OUT_CAP
+                    and os.environ.get("HPG_NO_PINNED_OUT") is None):
+                buf = torch.empty(n, dtype=F64, pin_memory=True)
+                buf.copy_(t, non_blocking=True)
+                cls._pinned_out_bytes += 8 * n
+                outs.append(None)
+                pend.append((len(outs) - 1, buf, n))
+            else:
+                outs.append(self.d2h(t, "many"))
+        fbuf = None
+        if flag is not None:
+            fbuf = self._pinned.get("flag_out")
+            if fbuf is None:
+                fbuf = self._pinned["flag_out"] = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            fbuf.copy_(flag.reshape(-1)[:1], non_blocking=True)
+        if pend or fbuf is not None:
+            torch.cuda.current_stream().synchronize()
+        for i, buf, n in pend:
+            arr = buf.numpy()
+            weakref.finalize(arr, cls._pinned_out_release, 8 * n)
+            outs[i] = arr
+        return outs, (int(fbuf[0]) if fbuf is not None else None)
+
     def d2h(self, t, tag):
         """Device tensor -> fresh host array (the reference returns fresh arrays)."""
         t = t.reshape(-1)
         n = t.numel()
-        if n < self._STAGE_MIN:
+        if n < self._PIN_OUT_MIN:
             out = np.empty(n)
             torch.from_numpy(out).copy_(t)
             return out
