@@ -625,12 +625,13 @@ class ObstacleDisc2D(_DeviceDisc):
     def exp_moments(self, psi):
         """((e^{-psi}, zeta_i), clamped) -- ``assembly.py:541-548``."""
         out, flag = self.exp_moments_t(self.h2d(psi, "psi"), out=self._dev("out_moments", self.ndof_psi))
-        res = self.d2h(out, "moments")
-        return res, bool(flag.item())
+        (res,), fl = self.d2h_many([out], flag=flag)
+        return res, bool(fl)
 
     def apply_D(self, psi, x):
         """``assembly.py:559-567``."""
-        y = self.apply_D_t(self.h2d(psi, "psi"), self.h2d(x, "x"), out=self._dev("out_y", self.ndof_psi))
+        psi_t, x_t = self.h2d_many([psi, x], ["psi", "x"])
+        y = self.apply_D_t(psi_t, x_t, out=self._dev("out_y", self.ndof_psi))
         return self.d2h(y, "y")
 
 
@@ -690,7 +691,8 @@ class GradientDisc2D(_DeviceDisc):
 
     def apply_D(self, psi, x):
         """``assembly.py:817-832``."""
-        y = self.apply_D_t(self.h2d(psi, "psi"), self.h2d(x, "x"), out=self._dev("out_y", self.ndof_psi))
+        psi_t, x_t = self.h2d_many([psi, x], ["psi", "x"])
+        y = self.apply_D_t(psi_t, x_t, out=self._dev("out_y", self.ndof_psi))
         return self.d2h(y, "y")
 
 
