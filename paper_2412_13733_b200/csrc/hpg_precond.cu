@@ -35,7 +35,11 @@ namespace {
 #endif
 constexpr int LU_THREADS = HPG_LU_THREADS;
 constexpr int LU_UCH = 64;     // trailing-update column chunk
-constexpr int LU_ULD = 72;     // its smem row stride (conflict-free B fragments)
+#ifndef HPG_LU_ULD
+#define HPG_LU_ULD 68
+#endif
+constexpr int LU_ULD = HPG_LU_ULD;     // its smem row stride: = 4 mod 16, so the B fragments B[c][r] of a
+                                       // half warp (r < 4) fall in 16 distinct 8-byte banks (72 gave 2-way conflicts)
 constexpr int SOLVE_THREADS = 128;
 
 // ---------------------------------------------------------------------------
@@ -378,7 +382,13 @@ __global__ void __launch_bounds__(LU_THREADS, HPG_LU_MINB) k_lu(PrecArgs A) {
 //    per-panel row interchanges of the right and left parts (k_lu's gather
 //    phase) are replaced by ONE permuting pass at the end.
 // (P_e = -D_e - T/alpha - beta E_e is formed by k_precond_transform first.)
-constexpr int LU2_T = 256, LU2_KB = 32, LU2_LDP = 33;
+// panel row stride in shared memory: = 4 mod 16, so the trailing update's A
+// fragments A[r][c] of a half warp fall in 16 distinct 8-byte banks (33 gave
+// up to 4-way conflicts: 368 M conflicts per factorisation in ncu)
+#ifndef HPG_LU2_LDP
+#define HPG_LU2_LDP 36
+#endif
+constexpr int LU2_T = 256, LU2_KB = 32, LU2_LDP = HPG_LU2_LDP;
 
 size_t lu2_smem(int nb) {
   return sizeof(double) * ((size_t)nb * LU2_LDP + LU2_KB * LU2_LDP + 2 * LU2_KB * LU_ULD + LU2_KB + 2) +
@@ -489,23 +499,19 @@ __global__ void __launch_bounds__(LU2_T, 2) k_lu2(PrecArgs A) {
     for (int k0 = 0; k0 < nb; k0 += KB) {
       const int kb = nb - k0 < KB ? nb - k0 : KB;
       PROF_MARK(0);
-      // (1) panel -> shared memory (coalesced) -> the owning thread's registers
-      bool bad = false;
-#pragma unroll 4
-      for (int idx = tid; idx < nb * KB; idx += LU2_T) {
-        const int i = idx >> 5, j = idx & 31;
-        double v = 0.0;
-        if (j < kb && sFpos[i] < 0) {
-          v = M[(size_t)i * nb + k0 + j];
-          bad |= !isfinite(v);
-        }
-        sP[i * LDP + j] = v;
-      }
-      if (bad && A.info) atomicOr(A.info, 1);
-      __syncthreads();
+      // (1) the row's panel entries straight into the owning thread's
+      //     registers (256 contiguous bytes per row: whole sectors)
       double a[KB];
+      {
+        bool bad = false;
+        const double* mrow = M + (size_t)tid * nb + k0;
 #pragma unroll
-      for (int j = 0; j < KB; ++j) a[j] = active ? sP[tid * LDP + j] : 0.0;
+        for (int j = 0; j < KB; ++j) {
+          a[j] = (active && j < kb) ? mrow[j] : 0.0;
+          bad |= !isfinite(a[j]);
+        }
+        if (bad && A.info) atomicOr(A.info, 1);
+      }
       PROF_MARK(7);
       // (2) the panel's columns
 #pragma unroll
@@ -578,11 +584,11 @@ __global__ void __launch_bounds__(LU2_T, 2) k_lu2(PrecArgs A) {
         for (int w = 0; w < warp; ++w) off += sCnt[w];
         if (active) sAct[off + __popc(bal & ((1u << lane) - 1))] = tid;
       }
-#pragma unroll 4
-      for (int idx = tid; idx < nb * KB; idx += LU2_T) {
-        const int i = idx >> 5, j = idx & 31;
-        const int fp = sFpos[i];
-        if (j < kb && (fp < 0 || fp >= k0)) M[(size_t)i * nb + k0 + j] = sP[i * LDP + j];
+      if (mine) {
+        double* mrow = M + (size_t)tid * nb + k0;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < kb) mrow[j] = a[j];
       }
       PROF_MARK(3);
       // (4) Linv = L11^{-1} (unit lower; L11 = the pivot rows in pivot order)
