@@ -696,70 +696,114 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 8) k_lu_solve(ElemArgs E, const
   }
   __syncthreads();
   // (2) forward, unit lower L, 32-row blocks: warp 0 solves the diagonal
-  //     block, then every thread updates one row below it (32 loads in flight)
-  for (int b0 = 0; b0 < nb; b0 += 32) {
-    const int bs = nb - b0 < 32 ? nb - b0 : 32;
-    if (warp == 0) {
-      // diagonal block through shared memory (row-contiguous, coalesced)
-      for (int i = 0; i < bs; ++i)
-        if (lane < bs) sD[i * 33 + lane] = __ldg(L + (size_t)(b0 + i) * nb + b0 + lane);
-      __syncwarp();
-      double xi = lane < bs ? sx[b0 + lane] : 0.0;
+  //     block, then every thread updates one row below it (32 loads in
+  //     flight).  The barrier wait on warp 0 dominated (ncu: 60 % of the warp
+  //     samples), so its critical path holds no global load of the diagonal:
+  //     the diagonal block after next is fetched by all threads (8 entries
+  //     each, registers) a round ahead into the second shared-memory buffer.
+  double* sDn = sD + 32 * 33 + ((nb + 1) / 2) * 1;   // second diagonal buffer (after the int row list)
+  auto diag_fetch = [&](int b0n, double (&dn)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + q * SOLVE_THREADS, i = idx >> 5, j = idx & 31;
+      dn[q] = (b0n >= 0 && b0n + i < nb && b0n + j < nb) ? __ldg(L + (size_t)(b0n + i) * nb + b0n + j) : 0.0;
+    }
+  };
+  auto diag_store = [&](double* dst, const double (&dn)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + q * SOLVE_THREADS;
+      dst[(idx >> 5) * 33 + (idx & 31)] = dn[q];
+    }
+  };
+  // Look-ahead: once block k of x is known, warp 0 alone updates the 32 rows
+  // of block k + 1 with it and goes straight on to solve block k + 1, while
+  // warps 1-3 apply block k to the rows beyond: one barrier per block, and
+  // the serial 32-step solve runs under the other warps' panel work.
+  auto row_update = [&](int i, int c0, int cs) {
+    // sx[i] -= sum_j L[i][c0 + j] sx[c0 + j], j < cs (two chains, k_lu_solve's order)
+    const double* Lr = L + (size_t)i * nb + c0;
+    double s0 = 0.0, s1 = 0.0;
+    if (cs == 32) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        s0 += __ldg(Lr + j) * sx[c0 + j];
+        s1 += __ldg(Lr + j + 1) * sx[c0 + j + 1];
+      }
+    } else {
+      for (int j = 0; j < cs; ++j) s0 += __ldg(Lr + j) * sx[c0 + j];
+    }
+    sx[i] -= s0 + s1;
+  };
+  auto solve_lower = [&](const double* sDc, int b0, int bs) {     // warp 0, unit lower
+    double xi = lane < bs ? sx[b0 + lane] : 0.0;
 #pragma unroll 8
-      for (int j = 0; j < 32; ++j) {
-        const double xj = __shfl_sync(~0u, xi, j);
-        if (j < lane && lane < bs) xi -= sD[lane * 33 + j] * xj;
-      }
-      if (lane < bs) sx[b0 + lane] = xi;
+    for (int j = 0; j < 32; ++j) {
+      const double xj = __shfl_sync(~0u, xi, j);
+      if (j < lane && lane < bs) xi -= sDc[lane * 33 + j] * xj;
     }
-    __syncthreads();
-    for (int i = b0 + bs + tid; i < nb; i += SOLVE_THREADS) {
-      const double* Lr = L + (size_t)i * nb + b0;
-      double s0 = 0.0, s1 = 0.0;
-      if (bs == 32) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          s0 += __ldg(Lr + j) * sx[b0 + j];
-          s1 += __ldg(Lr + j + 1) * sx[b0 + j + 1];
-        }
-      } else {
-        for (int j = 0; j < bs; ++j) s0 += __ldg(Lr + j) * sx[b0 + j];
-      }
-      sx[i] -= s0 + s1;
+    if (lane < bs) sx[b0 + lane] = xi;
+  };
+  auto solve_upper = [&](const double* sDc, int b0, int bs) {     // warp 0, non-unit upper
+    double xi = lane < bs ? sx[b0 + lane] : 0.0;
+    for (int j = bs - 1; j >= 0; --j) {
+      if (lane == j) xi = xi / sDc[j * 33 + j];
+      const double xj = __shfl_sync(~0u, xi, j);
+      if (lane < j) xi -= sDc[lane * 33 + j] * xj;
     }
-    __syncthreads();
-  }
-  // (3) backward, upper U (non-unit diagonal)
-  for (int b0 = ((nb - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
-    const int bs = nb - b0 < 32 ? nb - b0 : 32;
+    if (lane < bs) sx[b0 + lane] = xi;
+  };
+  double dn[8];
+  // forward: block 0
+  diag_fetch(0, dn);
+  diag_store(sD, dn);
+  diag_fetch(32 < nb ? 32 : -1, dn);
+  __syncthreads();
+  if (warp == 0) solve_lower(sD, 0, nb < 32 ? nb : 32);
+  diag_store(sDn, dn);
+  __syncthreads();
+  int cur = 1;                                   // buffer holding the NEXT block's diagonal
+  for (int b0 = 0; b0 + 32 < nb; b0 += 32) {
+    // x[b0 .. b0 + 32) is final; this round finishes block b1 = b0 + 32
+    const int b1 = b0 + 32, bs1 = nb - b1 < 32 ? nb - b1 : 32;
+    const double* sDc = cur ? sDn : sD;
+    diag_fetch(b1 + 32 < nb ? b1 + 32 : -1, dn);
     if (warp == 0) {
-      for (int i = 0; i < bs; ++i)
-        if (lane < bs) sD[i * 33 + lane] = __ldg(L + (size_t)(b0 + i) * nb + b0 + lane);
+      if (lane < bs1) row_update(b1 + lane, b0, 32);
       __syncwarp();
-      double xi = lane < bs ? sx[b0 + lane] : 0.0;
-      for (int j = bs - 1; j >= 0; --j) {
-        if (lane == j) xi = xi / sD[j * 33 + j];
-        const double xj = __shfl_sync(~0u, xi, j);
-        if (lane < j) xi -= sD[lane * 33 + j] * xj;
-      }
-      if (lane < bs) sx[b0 + lane] = xi;
+      solve_lower(sDc, b1, bs1);
+    } else {
+      for (int i = b1 + 32 + (tid - 32); i < nb; i += SOLVE_THREADS - 32) row_update(i, b0, 32);
     }
+    diag_store(cur ? sD : sDn, dn);
     __syncthreads();
-    for (int i = tid; i < b0; i += SOLVE_THREADS) {
-      const double* Ur = L + (size_t)i * nb + b0;
-      double s0 = 0.0, s1 = 0.0;
-      if (bs == 32) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          s0 += __ldg(Ur + j) * sx[b0 + j];
-          s1 += __ldg(Ur + j + 1) * sx[b0 + j + 1];
-        }
-      } else {
-        for (int j = 0; j < bs; ++j) s0 += __ldg(Ur + j) * sx[b0 + j];
-      }
-      sx[i] -= s0 + s1;
+    cur ^= 1;
+  }
+  // (3) backward, upper U (non-unit diagonal): last block first
+  const int bl = ((nb - 1) / 32) * 32, bsl = nb - bl;
+  diag_fetch(bl, dn);
+  diag_store(sD, dn);
+  diag_fetch(bl - 32, dn);
+  __syncthreads();
+  if (warp == 0) solve_upper(sD, bl, bsl);
+  diag_store(sDn, dn);
+  __syncthreads();
+  cur = 1;
+  for (int b0 = bl; b0 >= 32; b0 -= 32) {
+    // x[b0 .. b0 + bs) is final; this round finishes block b1 = b0 - 32
+    const int bs = nb - b0 < 32 ? nb - b0 : 32, b1 = b0 - 32;
+    const double* sDc = cur ? sDn : sD;
+    diag_fetch(b1 - 32, dn);
+    if (warp == 0) {
+      row_update(b1 + lane, b0, bs);
+      __syncwarp();
+      solve_upper(sDc, b1, 32);
+    } else {
+      for (int i = tid - 32; i < b1; i += SOLVE_THREADS - 32) row_update(i, b0, bs);
     }
+    diag_store(cur ? sD : sDn, dn);
     __syncthreads();
+    cur ^= 1;
   }
   for (int l = tid; l < nb; l += SOLVE_THREADS) {
     const int comp = l / n2, rem = l - comp * n2;
@@ -1015,7 +1059,7 @@ int launch_lu_solve(const ElemArgs& E, const double* lu, const int* ipiv, const 
   if (nb <= 8) return launch_lu_solve_warp_t<8>(E, lu, ipiv, nb, x, y, s);
   if (nb <= 16) return launch_lu_solve_warp_t<16>(E, lu, ipiv, nb, x, y, s);
   if (nb <= 32) return launch_lu_solve_warp_t<32>(E, lu, ipiv, nb, x, y, s);
-  const size_t smem = (sizeof(double) + sizeof(int)) * (size_t)nb + sizeof(double) * 32 * 33 + 16;
+  const size_t smem = (sizeof(double) + sizeof(int)) * (size_t)nb + sizeof(double) * 2 * 32 * 33 + 32;
   if (smem > (48u << 10)) {
     cudaError_t e = cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(HPG_ERR_CUDA, "cudaFuncSetAttribute(k_lu_solve)", e);
