@@ -16,7 +16,7 @@ from .mesh import Mesh1D, TensorMesh2D, uniform_mesh_1d, uniform_mesh_2d  # noqa
 
 def __getattr__(name):
     # torch-dependent modules load lazily so the CPU-only pieces import fast
-    if name in ("ObstacleDisc2D", "GradientDisc2D", "DeviceCellBlockMatrix"):
+    if name in ("ObstacleDisc2D", "GradientDisc2D", "DeviceCellBlockMatrix", "pinned_array"):
         from . import disc
         return getattr(disc, name)
     if name == "residual":

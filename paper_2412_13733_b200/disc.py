@@ -39,6 +39,17 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def pinned_array(shape):
+    """A float64 NumPy array in page-locked host memory.  Vectors a caller
+    keeps in such arrays are uploaded by ONE DMA straight from the array (no
+    staging copy: 0.14 ms instead of 0.22-0.33 ms for config 1's 7.4 MB
+    vector); the NumPy-facing methods return their large results in arrays
+    of this kind as well, so an iteration's vectors stay page-locked."""
+    n = int(np.prod(shape))
+    t = torch.empty(max(n, 1), dtype=F64, pin_memory=True)
+    return t.numpy()[:n].reshape(shape)
+
+
 def _require_cuda():
     if not torch.cuda.is_available():
         raise _lib.HpgError("paper_2412_13733_b200 needs a CUDA device (no CPU fallback)")
@@ -198,11 +209,22 @@ class _DeviceDisc:
             self._stage = st
         return st
 
-    def h2d(self, arr, tag):
+    def h2d(self, arr, tag, defer_sync=False):
         """Host array -> (reused) device tensor."""
         a = np.ascontiguousarray(arr, dtype=np.float64).reshape(-1)
         dev = self._dev("in_" + tag, a.size)
         n = a.size
+        if n >= self._PIN_OUT_MIN:
+            at = torch.from_numpy(a)
+            if at.is_pinned():
+                # page-locked source (pinned_array, or one of our own results):
+                # one DMA from the caller's memory; it must not change before
+                # the copy is done, so the transfer is finished here unless the
+                # caller synchronises before it returns anyway
+                dev.copy_(at, non_blocking=True)
+                if not defer_sync:
+                    torch.cuda.current_stream().synchronize()
+                return dev
         if n < self._STAGE_MIN:
             dev.copy_(torch.from_numpy(a))
             return dev
@@ -239,13 +261,15 @@ class _DeviceDisc:
     def _pinned_out_release(cls, nbytes):
         cls._pinned_out_bytes -= nbytes
 
-    def h2d_many(self, arrs, tags):
+    def h2d_many(self, arrs, tags, defer_sync=False):
         """Several host arrays -> device tensors.  Small / mid-size arrays
         (each below the chunking threshold) are packed into one page-locked
         staging buffer and uploaded by ONE DMA into one device buffer (the
         results are 256-byte aligned views of it); large ones go one by one
         through the pipelined path."""
         flat = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in arrs]
+        if all(a.size >= self._PIN_OUT_MIN and torch.from_numpy(a).is_pinned() for a in flat):
+            return [self.h2d(a, t, defer_sync=defer_sync) for a, t in zip(flat, tags)]
         if any(a.size >= self._CHUNK_MIN for a in flat) or sum(a.size for a in flat) < 64:
             return [self.h2d(a, t) for a, t in zip(flat, tags)]
         offs, total = [], 0
@@ -348,6 +372,10 @@ class _DeviceDisc:
         self._check_len(torch.from_numpy(a), self.ndof_psi, "x")
         cls = _DeviceDisc
         S = min(self._SLABS, self.ncx)
+        if n >= self._PIN_OUT_MIN and torch.from_numpy(a).is_pinned():
+            # page-locked x: upload straight from it, no slabs (d2h synchronises)
+            y = self.apply_cached_t(self.h2d(a, "x", defer_sync=True), out=self._dev("out_y", n), wcache=wcache)
+            return self.d2h(y, "y")
         if (S < 2 or n < 2 * self._STAGE_MIN or self.plan.path != 0
                 or cls._pinned_out_bytes + 8 * n > cls._PINNED_OUT_CAP
                 or os.environ.get("HPG_NO_PINNED_OUT") is not None):

@@ -197,3 +197,34 @@ def test_host_matvec_slab_pipeline(ncx, ncy, slabs):
     assert orc.rel_err(ya, P.obstacle_apply_D(psi, xa)) < TOL
     assert orc.rel_err(yb, P.obstacle_apply_D(psi, xb)) < TOL
     assert orc.rel_err(ya, ya1) < 1e-13
+
+
+@pytest.mark.parametrize("cfg_name,ncells", [("c1", 64), ("c3", 2), ("c4p4", 64)])
+def test_page_locked_inputs(cfg_name, ncells):
+    """Inputs kept in page-locked arrays (``disc.pinned_array``, or results of
+    earlier calls) are uploaded straight from the caller's memory: same
+    results as pageable inputs, and a caller may overwrite its array as soon
+    as a call has returned (``assemble_D`` keeps no reference to psi's memory)."""
+    from paper_2412_13733_b200.disc import pinned_array
+    from paper_2412_13733_b200.proximal import residual
+    cfg, d, P, inp, dev = build(cfg_name, ncells=ncells)
+    pin = {}
+    for k in ("psi", "psi_prev", "u", "x"):
+        pin[k] = pinned_array(inp[k].shape)
+        pin[k][...] = inp[k]
+    alpha = cfg.alphas[0]
+    a = residual(d, alpha, inp["psi_prev"], inp["u"], inp["psi"])
+    b = residual(d, alpha, pin["psi_prev"], pin["u"], pin["psi"])
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    Dm = d.assemble_D(pin["psi"])
+    y_ref = d.assemble_D(inp["psi"]) @ inp["x"]
+    pin["psi"][...] = 123.0                       # the call has returned: D must not change
+    y = Dm @ pin["x"]
+    # (1e-13: pageable vectors of a large mesh go through the slab pipeline,
+    # whose slabs may run on the one-wave kernel -- another summation order
+    # for the cells the streaming kernel splits between two warps)
+    assert orc.rel_err(y, y_ref) < 1e-13
+    # a result (page-locked) fed back as an input
+    y2 = Dm @ y
+    assert orc.rel_err(y2, Dm @ np.array(y, copy=True)) < 1e-13
+    assert np.array_equal(d.apply_D(inp["psi"], pin["x"]), d.apply_D(inp["psi"], inp["x"]))
