@@ -185,7 +185,7 @@ size_t blockrow_smem(const hpgPlan_st* P, int* pk_smem) {
   const int threads = 128;
   const size_t zs = sizeof(double) * (size_t)P->NT * P->QT * 64;
   const size_t pks = sizeof(double) * (size_t)P->n * P->NT * 2 * P->QT * 32;
-  const size_t so = sizeof(double) * (size_t)(8 * P->NT) * (8 * P->NT + 1);
+  const size_t so = sizeof(double) * (size_t)(8 * P->NT) * blockrow_ldo(8 * P->NT);
   size_t smem = pks + (zs + so) * (threads / 32);
   *pk_smem = 1;
   if (smem > ((size_t)200 << 10) && P->NT <= 4) {
@@ -808,6 +808,11 @@ static int blocks_impl(hpgPlan P, const double* wcache, double* blocks, int c0, 
     case 12: fn = (void*)k_blockrow<12>; break;
     default: fn = nullptr;
   }
+  // hot shapes with the quadrature tile count at compile time
+  if (P->NT == 2 && P->QT == 3) fn = (void*)k_blockrow<2, 3>;        // config 1, Gauss rule
+  if (P->NT == 2 && P->QT == 5) fn = (void*)k_blockrow<2, 5>;        // config 1, reference rule
+  if (P->NT == 3 && P->QT == 5) fn = (void*)k_blockrow<3, 5>;        // config 2
+  if (P->NT == 1 && P->QT == 2) fn = (void*)k_blockrow<1, 2>;        // config 0
   if (fn == nullptr) return fail(HPG_ERR_UNSUPPORTED, "block-row kernel supports n <= 96");
   if (smem > (48u << 10)) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;

@@ -39,14 +39,21 @@ struct BArgs {
 
 constexpr int BR_MAXACC = 24;   // 8x8 accumulator tiles per warp
 
-template <int NT>
+// output staging tile row stride: = 8 mod 16, so the double2 stores of the
+// accumulator fragments (j = 8 mt + r, k = 8 nt + 2c) of a quarter warp fall
+// in distinct 16-byte bank groups (NP + 1 gave 31 M conflicts at config 1)
+__host__ __device__ constexpr int blockrow_ldo(int NP) { return ((NP + 7) / 16) * 16 + 8; }
+
+// QTC > 0: the number of quadrature tiles at compile time (hot shapes: the
+// contraction loops unroll); 0: read from the arguments.
+template <int NT, int QTC = 0>
 __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
   // k-tile columns per warp pass: all NT for the small (warp-per-item) shapes
   constexpr int NC = NT <= 4 ? NT : (BR_MAXACC / NT > 0 ? BR_MAXACC / NT : 1);
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int r = lane >> 2, c = lane & 3;
-  const int n = B.n, QT = B.QT, QK = 2 * QT, QP = 8 * QT;
+  const int n = B.n, QT = QTC > 0 ? QTC : B.QT, QK = 2 * QT, QP = 8 * QT;
   const int zsize = NT * QT * 64;
   const long long items = (long long)B.ncell * B.nf * n;
   // group = the threads sharing one item
@@ -61,7 +68,7 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
   const double* PKb = B.pk_smem ? sPK : B.PKG;
   double* sZ = smem + pk_len + (size_t)gid * zsize;
   // per-group output staging tile (NP x NP), written back as a contiguous block row
-  const int NP = 8 * NT, LDO = NP + 1;
+  constexpr int NP = 8 * NT, LDO = blockrow_ldo(NP);
   double* sO = smem + pk_len + (size_t)(B.per_warp ? nwarps : 1) * zsize + (size_t)gid * NP * LDO;
   __syncthreads();
   for (long long it = (long long)blockIdx.x * (B.per_warp ? nwarps : 1) + gid; it < items;
@@ -78,6 +85,7 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
       double z[2] = {0.0, 0.0};
       const int j = 8 * mt + r;
       const double* grow = B.G + ((long long)a * n + (j < n ? j : 0)) * QP;
+#pragma unroll (QTC > 0 ? 2 * QTC : 1)
       for (int ks = 0; ks < QK; ++ks) {
         const int g = 8 * (ks >> 1) + 2 * c + (ks & 1);
         const double av = (j < n) ? __ldg(grow + g) : 0.0;
@@ -104,6 +112,7 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
         for (int ci = 0; ci < NC; ++ci)
 #pragma unroll
           for (int mt = 0; mt < NT; ++mt) acc[ci][mt][0] = acc[ci][mt][1] = 0.0;
+#pragma unroll (QTC > 0 ? QTC : 1)
         for (int ht = 0; ht < QT; ++ht) {
           double bf[NC][2];
 #pragma unroll
@@ -133,8 +142,7 @@ __global__ void __launch_bounds__(256) k_blockrow(BArgs B) {
 #pragma unroll
           for (int mt = 0; mt < NT; ++mt) {
             const int j = 8 * mt + r, k = 8 * nt + 2 * c;
-            sO[j * LDO + k] = acc[ci][mt][0] * wab;
-            sO[j * LDO + k + 1] = acc[ci][mt][1] * wab;
+            *reinterpret_cast<double2*>(sO + j * LDO + k) = make_double2(acc[ci][mt][0] * wab, acc[ci][mt][1] * wab);
           }
         }
       }
