@@ -299,8 +299,8 @@ def config_dict(cfg, rule, cached=None):
 
 # dram bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (cold caches: ncu flushes L2 between replays), see profiles/
-NCU_TRAFFIC = {("c1", "gauss"): (26275072.0, "profiles/r01e_ncu_full_c1_apply.txt"),
-               ("c4p6", "gauss"): (90302464.0 + 22354176.0, "profiles/r01b_ncu_full_c4p6_lowp.txt")}
+NCU_TRAFFIC = {("c1", "gauss"): (26274304.0 + 0.0, "profiles/r02c_ncu_full_c1_stream_cold.txt"),
+               ("c4p6", "gauss"): (90812928.0 + 22752256.0, "profiles/r02a_ncu_full_c4p6_lowp.txt")}
 
 
 # ---------------------------------------------------------------------------
