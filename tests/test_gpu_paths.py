@@ -228,3 +228,25 @@ def test_page_locked_inputs(cfg_name, ncells):
     y2 = Dm @ y
     assert orc.rel_err(y2, Dm @ np.array(y, copy=True)) < 1e-13
     assert np.array_equal(d.apply_D(inp["psi"], pin["x"]), d.apply_D(inp["psi"], inp["x"]))
+
+
+def test_host_matvec_slabs_gradient():
+    """The slab pipeline on a gradient plan (two stacked components: a slab is
+    two row ranges) with the warp-per-cell apply: 56 x 56 cells, p = 8."""
+    from types import SimpleNamespace
+    from paper_2412_13733_b200 import disc as D
+    from paper_2412_13733_b200.mesh import uniform_mesh_2d
+    p, nc = 8, 56
+    rng = np.random.default_rng(5)
+    d = D.GradientDisc2D(uniform_mesh_2d(0.0, 1.0, nc, p), 1.0, 0.7, rule="gauss", nq=12)
+    assert d.plan.path == 0 and d.ndof_psi >= 2 * d._STAGE_MIN
+    t = d.tables
+    P = orc.Problem("gradient", d.xpts, d.ypts, p, SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
+    psi = 0.3 * rng.standard_normal(d.ndof_psi)
+    x = rng.standard_normal(d.ndof_psi)
+    Dm = d.assemble_D(psi)
+    ry = P.gradient_apply_D(psi, x, P.sample(0.7))
+    for slabs in (2, 3, 1):
+        d._SLABS = slabs
+        y = Dm @ x
+        assert orc.rel_err(y, ry) < TOL, slabs
