@@ -128,8 +128,8 @@ def test_lowp_flag_and_nan_semantics(cfg_name, bad):
         assert orc.rel_err(a[ok], b[ok]) < TOL
 
 
-@pytest.mark.parametrize("ncx,ncy", [(64, 64), (61, 63), (59, 61)])
-def test_streaming_cached_apply(ncx, ncy):
+@pytest.mark.parametrize("ncx,ncy,nq", [(64, 64, 24), (61, 63, 24), (59, 61, 24), (64, 62, 16), (63, 61, 10)])
+def test_streaming_cached_apply(ncx, ncy, nq):
     """Config-1 shaped cached Jacobian apply on the persistent streaming
     kernel (k_stream: equal row-tile runs per warp, cells split between two
     warps summed through shared memory) vs the oracle and vs the one-wave
@@ -145,7 +145,7 @@ def test_streaming_cached_apply(ncx, ncy):
     xs = np.concatenate([[0.0], np.cumsum(rng.uniform(0.5, 1.5, ncx))]); xs /= xs[-1]
     ys = np.concatenate([[0.0], np.cumsum(rng.uniform(0.5, 1.5, ncy))]); ys /= ys[-1]
     mesh = TensorMesh2D(Mesh1D(xs, np.full(ncx, p)), Mesh1D(ys, np.full(ncy, p)))
-    d = D.ObstacleDisc2D(mesh, 1.0, phi_sin, rule="gauss", nq=24)
+    d = D.ObstacleDisc2D(mesh, 1.0, phi_sin, rule="gauss", nq=nq)   # nq = 24 / 16: 3 / 2 point tiles
     t = d.tables
     P = orc.Problem("obstacle", d.xpts, d.ypts, p, SimpleNamespace(S=t.S, T=t.T, Su=t.Su, Tu=t.Tu, xi=t.xi, nq=t.nq))
     psi = 0.5 * rng.standard_normal(d.ndof_psi)
@@ -250,3 +250,31 @@ def test_host_matvec_slabs_gradient():
         d._SLABS = slabs
         y = Dm @ x
         assert orc.rel_err(y, ry) < TOL, slabs
+
+
+@pytest.mark.parametrize("ranges", [[(0, 4000), (4000, 4096)], [(0, 96), (96, 4096)], [(0, 1), (1, 2049), (2049, 4096)]])
+def test_apply_cached_range(ranges):
+    """hpgApplyCachedRange: disjoint cell ranges (streaming kernel with a
+    non-zero first cell, one-wave kernel, a single cell) tile the full apply;
+    cells outside a range are left untouched."""
+    import torch
+    from paper_2412_13733_b200 import _lib, disc as D
+    cfg, d, P, inp, dev = build("c1")
+    d.exp_moments_t(dev["psi"], wcache=True)
+    full = d.apply_cached_t(dev["x"]).cpu().numpy()
+    y = torch.full_like(dev["x"], -7.0)
+    for lo, hi in ranges:
+        _lib.call("hpgApplyCachedRange", d.plan.handle, D._vp(d._wcache), D._vp(dev["x"]), D._vp(y), lo, hi,
+                  D._stream())
+        got = y.cpu().numpy()
+        n = d.n
+        cells = np.arange(lo, hi)
+        # x-major cell order: cell = cx * ncy + cy; its tile rows / columns
+        tile = got.reshape(d.ncx * n, d.ncy * n)
+        ref = full.reshape(d.ncx * n, d.ncy * n)
+        cx, cy = cells[0] // d.ncy, cells[0] % d.ncy
+        assert orc.rel_err(tile[cx * n:(cx + 1) * n, cy * n:(cy + 1) * n], ref[cx * n:(cx + 1) * n, cy * n:(cy + 1) * n]) < 1e-13
+    assert orc.rel_err(y.cpu().numpy(), full) < 1e-13          # the ranges tiled everything
+    with pytest.raises(ValueError):                            # HPG_ERR_ARG
+        _lib.call("hpgApplyCachedRange", d.plan.handle, D._vp(d._wcache), D._vp(dev["x"]), D._vp(y), 10, 5000,
+                  D._stream())
