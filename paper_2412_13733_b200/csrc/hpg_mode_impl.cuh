@@ -59,7 +59,9 @@ int launch_warp_t(const ElemArgs& A, cudaStream_t s) {
     // (a cell then spans at most two warps' row-tile runs)
     const bool stream_ok = getenv("HPG_NO_STREAM") == nullptr;
     const int nsm = device_sm_count();
-    if (stream_ok && (A.N - A.e0) / nsm / 4 >= 2 * StreamCfg<NT, QT, MODE>::MW) return launch_stream_t<NT, QT, MODE>(A, nsm, s);
+    // (its in-cell offsets are 32-bit)
+    if (stream_ok && (A.N - A.e0) / nsm / 4 >= 2 * StreamCfg<NT, QT, MODE>::MW && 8 * NT * A.ld < (1LL << 31))
+      return launch_stream_t<NT, QT, MODE>(A, nsm, s);
   }
   constexpr int NP = 8 * NT, QP = 8 * QT;
   constexpr int NSTAGE = WarpCfg<NT, QT, MODE>::REGX ? 0 : TR::NIN;

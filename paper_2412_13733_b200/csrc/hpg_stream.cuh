@@ -123,6 +123,21 @@ k_stream(ElemArgs A) {
     if (cy < 0) { --cx; cy += A.ncy; }
     if (cy >= A.ncy) { ++cx; cy -= A.ncy; }
   };
+  // lane-invariant tile geometry: the fragment rows this lane touches are
+  // a_q = 8 (q >> 1) + 2c + (q & 1), q < NK (x loads: q = k-step; stores:
+  // q = 2 at + j), the columns b_nt = 8 nt + r; their element offsets inside
+  // a cell (32-bit: the launcher checks the vector length) and in-range masks
+  // are computed once, so an item's addresses are one cell base plus these
+  int ro[NK];
+  bool okr[NK], okc[NT];
+#pragma unroll
+  for (int q = 0; q < NK; ++q) {
+    const int a = 8 * (q >> 1) + 2 * c + (q & 1);
+    ro[q] = a * (int)A.ld + r;
+    okr[q] = a < A.n;
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) okc[nt] = 8 * nt + r < A.n;
   using XFrag = double[NIN][NK][NT];
   XFrag X, Xn;
   double hxv = 0.0, hyv = 0.0, hxn = 0.0, hyn = 0.0;
@@ -138,14 +153,10 @@ k_stream(ElemArgs A) {
       field_src<MODE>(A, f, src, comp);
       src += comp * A.ncomp + psi_index(A, cx, cy, 0, 0);
 #pragma unroll
-      for (int ks = 0; ks < NK; ++ks) {
-        const int a = 8 * (ks >> 1) + 2 * c + (ks & 1);
+      for (int ks = 0; ks < NK; ++ks)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int b = 8 * nt + r;
-          Xd[f][ks][nt] = (a < A.n && b < A.n) ? __ldg(src + (long long)a * A.ld + b) : 0.0;
-        }
-      }
+        for (int nt = 0; nt < NT; ++nt)
+          Xd[f][ks][nt] = (okr[ks] && okc[nt]) ? __ldg(src + ro[ks] + 8 * nt) : 0.0;
     }
   };
   auto item_rb = [&](int i) { return lo > i * QT ? lo - i * QT : 0; };
@@ -288,6 +299,7 @@ k_stream(ElemArgs A) {
             }
       }
       // M[a][b] = w_a w_b Y[b][a] (write_moment's order of operations)
+      double* dst0 = A.out + psi_index(A, cx, cy, 0, 0);
 #pragma unroll
       for (int o = 0; o < NOUT; ++o)
 #pragma unroll
@@ -296,10 +308,10 @@ k_stream(ElemArgs A) {
           for (int at = 0; at < NT; ++at)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-              const int a = 8 * at + 2 * c + j, b = 8 * bt + r;
-              if (a < A.n && b < A.n) {
-                const double wa = hxv * sInv[a], wb = hyv * sInv[b];
-                A.out[(long long)o * A.ncomp + psi_index(A, cx, cy, a, b)] = (wa * Y[o][bt][at][j]) * wb;
+              const int q = 2 * at + j;
+              if (okr[q] && okc[bt]) {
+                const double wa = hxv * sInv[8 * at + 2 * c + j], wb = hyv * sInv[8 * bt + r];
+                dst0[(long long)o * A.ncomp + ro[q] + 8 * bt] = (wa * Y[o][bt][at][j]) * wb;
               }
             }
     }
