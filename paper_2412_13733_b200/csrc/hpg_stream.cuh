@@ -240,23 +240,16 @@ k_stream(ElemArgs A) {
       // R = T W^T (even / odd k-step chains, summed), Y += R T[:,rt]^T
 #pragma unroll
       for (int o = 0; o < NOUT; ++o) {
-        double R[NT][2], R1[NT][2];
+        double R[NT][2];
 #pragma unroll
-        for (int bt = 0; bt < NT; ++bt) R[bt][0] = R[bt][1] = R1[bt][0] = R1[bt][1] = 0.0;
+        for (int bt = 0; bt < NT; ++bt) R[bt][0] = R[bt][1] = 0.0;
+        // (one chain per tile: the even / odd split of k_warp costs 2 NT DADDs
+        // per row tile on the pipe the DMMAs use, and three warps per
+        // scheduler cover the chain latency)
 #pragma unroll
-        for (int ks = 0; ks < QK; ks += 2) {
+        for (int ks = 0; ks < QK; ++ks)
 #pragma unroll
-          for (int bt = 0; bt < NT; ++bt) {
-            dmma(R[bt], Tr[bt][ks], Vw[o][ks >> 1][0]);
-            dmma(R1[bt], Tr[bt][ks + 1], Vw[o][ks >> 1][1]);
-          }
-          HPG_FENCE();
-        }
-#pragma unroll
-        for (int bt = 0; bt < NT; ++bt) {
-          R[bt][0] += R1[bt][0];
-          R[bt][1] += R1[bt][1];
-        }
+          for (int bt = 0; bt < NT; ++bt) dmma(R[bt], Tr[bt][ks], Vw[o][ks >> 1][ks & 1]);
 #pragma unroll
         for (int k2 = 0; k2 < 2; ++k2) {
 #pragma unroll
@@ -300,6 +293,11 @@ k_stream(ElemArgs A) {
       }
       // M[a][b] = w_a w_b Y[b][a] (write_moment's order of operations)
       double* dst0 = A.out + psi_index(A, cx, cy, 0, 0);
+      double wa[NK], wb[NT];
+#pragma unroll
+      for (int q = 0; q < NK; ++q) wa[q] = hxv * sInv[8 * (q >> 1) + 2 * c + (q & 1)];
+#pragma unroll
+      for (int bt = 0; bt < NT; ++bt) wb[bt] = hyv * sInv[8 * bt + r];
 #pragma unroll
       for (int o = 0; o < NOUT; ++o)
 #pragma unroll
@@ -309,10 +307,8 @@ k_stream(ElemArgs A) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const int q = 2 * at + j;
-              if (okr[q] && okc[bt]) {
-                const double wa = hxv * sInv[8 * at + 2 * c + j], wb = hyv * sInv[8 * bt + r];
-                dst0[(long long)o * A.ncomp + ro[q] + 8 * bt] = (wa * Y[o][bt][at][j]) * wb;
-              }
+              if (okr[q] && okc[bt])
+                dst0[(long long)o * A.ncomp + ro[q] + 8 * bt] = (wa[q] * Y[o][bt][at][j]) * wb[bt];
             }
     }
     if (more) {
