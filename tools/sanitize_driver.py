@@ -2,7 +2,9 @@
 (memcheck / racecheck / synccheck): config 0 (both rules), config 4's p = 2 on
 a 16 x 16 mesh, config 1's degree on 2 x 2 cells (warp path, generated U
 passes), a gradient disc (CTA path), element blocks, the per-cell
-preconditioner, the Schur operator and the device GMRES graph.
+preconditioner, the Schur operator, the device GMRES graph, and config 1's
+degree on 60 x 60 cells (streaming apply, cell ranges, host slab pipeline,
+row-per-thread LU and look-ahead solve).
 
     compute-sanitizer --tool memcheck python tools/sanitize_driver.py
 """
@@ -44,6 +46,34 @@ def run(kind, nc, p, rule, nq=None, blocks=True, solve=True):
     print(f"ok {kind} nc={nc} p={p} {rule} path={d.plan.path} splits={d.plan.splits}", flush=True)
 
 
+def run_stream():
+    """Config 1's degree on 60 x 60 cells: the persistent streaming apply
+    (k_stream, split cells through shared memory + named barriers), the cell
+    range entry, the host slab pipeline and page-locked inputs / results."""
+    from paper_2412_13733_b200 import _lib
+    from paper_2412_13733_b200.disc import pinned_array
+    nc, p = 60, 16
+    d = D.ObstacleDisc2D(uniform_mesh_2d(0.0, 1.0, nc, p), 1.0, phi_sin, rule="gauss", nq=24)
+    psi, u, x, _ = make_inputs("obstacle", nc, nc, p, seed=2)
+    Dm = d.assemble_D(psi)
+    y = Dm @ x                                   # pageable x: two slabs (hpgApplyCachedHostSlab)
+    xp = pinned_array(x.shape)
+    xp[...] = x
+    y2 = Dm @ xp                                 # page-locked x: one DMA, whole vector (k_stream)
+    assert np.allclose(y, y2, rtol=1e-12, atol=1e-14)
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.zeros_like(xt)
+    for lo, hi in ((0, 40), (40, d.plan.ncells)):
+        _lib.call("hpgApplyCachedRange", d.plan.handle, D._vp(Dm._w), D._vp(xt), D._vp(yt), lo, hi, D._stream())
+    assert np.allclose(yt.cpu().numpy(), y, rtol=1e-12, atol=1e-14)
+    M = D.DeviceCellBlockPreconditioner.from_blocks(
+        d, torch.eye(d.n * d.n, dtype=torch.float64, device="cuda").repeat(d.plan.ncells, 1, 1)
+        + 0.01 * torch.randn(d.plan.ncells, d.n * d.n, d.n * d.n, dtype=torch.float64, device="cuda"))
+    M.apply_t(xt)                                # k_lu2 + look-ahead k_lu_solve
+    torch.cuda.synchronize()
+    print(f"ok stream nc={nc} p={p} path={d.plan.path}", flush=True)
+
+
 if __name__ == "__main__":
     run("obstacle", 4, 8, "gauss", 12)          # config 0
     run("obstacle", 4, 8, "reference")
@@ -52,4 +82,5 @@ if __name__ == "__main__":
     run("obstacle", 2, 16, "gauss", 24)         # config 1 degree (k_warp)
     run("gradient", 2, 6, "gauss", 9)           # gradient, CTA path
     run("gradient", 3, 3, "reference")
+    run_stream()
     print("sanitize driver done")
